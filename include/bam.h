@@ -1,0 +1,184 @@
+/* bam.h -- C ABI of libbam.so, the B200-native (sm_100a) hot path of Cornstarch's
+ * token workload-balanced context-parallel attention under bitfield masks.
+ *
+ * The reference (/root/reference/pkg, Python package `mmplan`) has no FFI; its
+ * hot-path interface is the Python API listed below.  Each entry point names
+ * the reference function (file:line, relative to /root/reference/pkg) whose
+ * work it replaces.  The Python host layer (paper_2503_11367_b200.mask /
+ * .balance / .attention) binds these through ctypes with the same names,
+ * argument meanings and exceptions as the reference.
+ *
+ * Conventions (all entry points):
+ *   - return 0 on success, otherwise a BamStatus code; bam_last_error() gives
+ *     a thread-local message;
+ *   - every pointer argument is a caller-allocated DEVICE buffer unless the
+ *     comment says "host";
+ *   - work is enqueued on `stream` (a cudaStream_t passed as void*) and is
+ *     asynchronous; nothing allocates device memory and nothing synchronises
+ *     except where the comment says so;
+ *   - re-entrant: no global mutable state besides the per-thread error text.
+ */
+#ifndef BAM_H_
+#define BAM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum BamStatus {
+  BAM_OK = 0,
+  BAM_INVALID_ARGUMENT = 1,
+  BAM_CUDA_ERROR = 2,
+  BAM_UNSUPPORTED = 3,
+  BAM_BUDGET_EXCEEDED = 4
+} BamStatus;
+
+#define BAM_SUMMARY_ALL_TEXT 1
+#define BAM_SUMMARY_NO_TEXT 2
+
+/* Per-block summary of descriptors. */
+typedef struct BamBlockSummary {
+  int64_t or_bits;   /* OR of the block's descriptors  */
+  int64_t and_bits;  /* AND of the block's descriptors */
+  int64_t lo, hi;    /* token range [lo, hi)           */
+  int32_t flags;     /* BAM_SUMMARY_* bits              */
+  int32_t pad;
+} BamBlockSummary;
+
+const char* bam_last_error(void);
+int bam_version(void);
+
+/* ---- bitfield masks (reference src/mmplan/mask.py) ------------------------ */
+
+/* build_bitfield (mask.py:71-103): expand per-segment descriptors to one per
+ * token.  seg_desc[i] is segment i's descriptor, seg_end[i] its exclusive end
+ * token (prefix sum of counts).  desc[T] out. */
+int bam_mask_expand(const int64_t* seg_desc, const int64_t* seg_end, int32_t nseg, int64_t T,
+                    int64_t* desc, void* stream);
+
+/* BitfieldMask.validate (mask.py:53-68), token checks in reference order.
+ * err (device, 1 x u64) receives min over failing tokens of (t << 2 | kind),
+ * kind 1 = reserved control bits, 2 = zero descriptor, 3 = pure modality
+ * popcount != 1; all ones when every token is valid.  (The range check and
+ * the modality-count check are done by the host before the int64 copy.) */
+int bam_mask_validate(const int64_t* desc, int64_t T, unsigned long long* err, void* stream);
+
+/* Per-block OR/AND/text summaries for blocks of `block_size` tokens. */
+int bam_block_summarize(const int64_t* desc, int64_t T, int64_t block_size,
+                        BamBlockSummary* out, void* stream);
+
+/* block_workloads (mask.py:168-188) / _classify_pair (mask.py:132-165):
+ * classes[nb*nb] (0 skip, 1 full, 2 partial; row = query block) and
+ * W[nb] = non-skip tiles per query block.  Bit-exact with the reference. */
+int bam_classify(const int64_t* desc, const BamBlockSummary* summaries, int64_t nb,
+                 uint8_t* classes, int32_t* W, void* stream);
+
+/* Tile lists for the attention kernels over the local query blocks q_gid[nq]:
+ * CSR rows (entry kb << 2 | class, kb ascending) and CSC columns over all nb
+ * key blocks (entry j << 2 | class, j = local q index ascending).
+ * row_off[nq+1], col_off[nb+1]; row_tiles / col_tiles may be NULL (counts and
+ * offsets only).  Counts: row_cnt[nq], col_cnt[nb]. */
+int bam_build_tile_lists(const uint8_t* classes, int64_t nb, const int32_t* q_gid, int32_t nq,
+                         int32_t* row_cnt, int32_t* row_off, int32_t* row_tiles, int32_t* col_cnt,
+                         int32_t* col_off, int32_t* col_tiles, void* stream);
+
+/* ---- distribution (reference src/mmplan/balance.py) ----------------------- */
+
+/* lpt_distribute (balance.py:58-76), also the list scheduler of
+ * intra_schedule (balance.py:251-259): items sorted by (-w, index), each to
+ * argmin (load, unit).  0 <= w[i] < 2^31.
+ * Outputs: owner[n]; flat[n] = items grouped by unit, each unit's items in
+ * assignment order, unit g occupying flat[off[g] .. off[g+1]); off[G+1];
+ * loads[G].  workspace: >= bam_lpt_workspace_bytes(n) bytes (device). */
+int64_t bam_lpt_workspace_bytes(int64_t n);
+int bam_lpt_assign(const int32_t* w, int64_t n, int32_t G, int32_t* owner, int32_t* flat,
+                   int32_t* off, int64_t* loads, void* workspace, void* stream);
+
+/* zigzag_distribute (balance.py:79-102) and the naive contiguous split
+ * (BASELINE.json config 5; not in the reference).  Same outputs as LPT. */
+int bam_zigzag_assign(const int32_t* w, int64_t n, int32_t G, int32_t* owner, int32_t* flat,
+                      int32_t* off, int64_t* loads, void* stream);
+int bam_contiguous_assign(const int32_t* w, int64_t n, int32_t G, int32_t* owner, int32_t* flat,
+                          int32_t* off, int64_t* loads, void* stream);
+
+/* split_block pieces for intra_schedule (balance.py:217-220, 237-245): for
+ * block b with workload w[b], ceil(w/s) pieces of size s except a final
+ * remainder.  piece_off[n+1] (exclusive scan of piece counts) is produced by
+ * bam_split_count; bam_split_fill writes piece_size / piece_block /
+ * piece_index in (block, index) order. */
+int bam_split_count(const int32_t* w, int64_t n, int32_t s, int32_t* piece_cnt,
+                    int32_t* piece_off, void* stream);
+int bam_split_fill(const int32_t* w, int64_t n, int32_t s, const int32_t* piece_off,
+                   int32_t* piece_size, int32_t* piece_block, int32_t* piece_index, void* stream);
+
+/* ilp_optimal (balance.py:124-192): exact branch-and-bound makespan, then
+ * the lexicographically smallest assignment.  HOST pointers; synchronous.
+ * Returns BAM_BUDGET_EXCEEDED past 14 blocks or 4 GPUs (balance.py:23-24). */
+int bam_ilp_optimal(const int64_t* w, int32_t n, int32_t G, int32_t* assignment,
+                    int64_t* makespan);
+
+/* ---- attention (absent in the reference) ---------------- */
+
+/* Forward, bitfield-masked, 128x128 tiles, head_dim 128, bf16 in / fp32 acc.
+ * Query rows are the local query blocks (q_gid) in local order; keys/values
+ * are all nb global blocks stored at block-row k_row[kb] of k/v. */
+typedef struct BamAttnFwdParams {
+  const void* q;            /* bf16 [nq*128, Hq, 128]            */
+  const void* k;            /* bf16 [k_rows*128, Hkv, 128]       */
+  const void* v;            /* bf16 [k_rows*128, Hkv, 128]       */
+  void* o;                  /* bf16 [nq*128, Hq, 128] out        */
+  float* lse;               /* fp32 [Hq, nq*128] out (natural log) */
+  const int64_t* desc;      /* int64 [nb*128] descriptors         */
+  const int32_t* q_gid;     /* [nq]                               */
+  const int32_t* k_row;     /* [nb]                               */
+  const int32_t* row_off;   /* [nq+1] CSR from bam_build_tile_lists */
+  const int32_t* row_tiles; /* kb << 2 | class                    */
+  const int32_t* order;     /* [nq] local q-block processing order (heavy first), or NULL */
+  int32_t nq, nb, k_rows, Hq, Hkv;
+  float scale;              /* softmax scale, usually 1/sqrt(128) */
+} BamAttnFwdParams;
+int bam_attn_fwd(const BamAttnFwdParams* p, void* stream);
+
+/* Backward.  dq (bf16) for the local rows; dk/dv fp32 partial gradients for
+ * every key row of k/v (the contributions of the local queries; summed over
+ * CP ranks by a reduce-scatter).  delta ([Hq, nq*128] fp32) and dq_acc
+ * ([nq*128, Hq, 128] fp32) are caller workspaces. */
+typedef struct BamAttnBwdParams {
+  const void* q;
+  const void* k;
+  const void* v;
+  const void* o;
+  const void* dout;         /* bf16 [nq*128, Hq, 128]             */
+  const float* lse;         /* [Hq, nq*128] from the forward      */
+  float* delta;             /* workspace [Hq, nq*128]             */
+  float* dq_acc;            /* workspace [nq*128, Hq, 128]        */
+  void* dq;                 /* bf16 [nq*128, Hq, 128] out         */
+  float* dk;                /* fp32 [k_rows*128, Hkv, 128] out    */
+  float* dv;                /* fp32 [k_rows*128, Hkv, 128] out    */
+  const int64_t* desc;
+  const int32_t* q_gid;
+  const int32_t* k_row;
+  const int32_t* col_off;   /* [nb+1] CSC from bam_build_tile_lists */
+  const int32_t* col_tiles; /* j << 2 | class                     */
+  const int32_t* order;     /* [nb] key-block processing order, or NULL */
+  int32_t nq, nb, k_rows, Hq, Hkv;
+  float scale;
+} BamAttnBwdParams;
+int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
+
+/* fp32 -> bf16 conversion (dk/dv partials to the bf16 gradient layout). */
+int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+/* One-CTA tcgen05/TMA self test: out[3][128][128] fp32 =
+ * {A*B^T (SS, both K-major), A*V (TS: A from TMEM, V MN-major),
+ *  X^T*V (SS, A MN-major)} for bf16 inputs a, b, v, x of [128,128]. */
+int bam_selftest_umma(const void* a, const void* b, const void* v, const void* x, float* out,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BAM_H_ */

@@ -1,0 +1,119 @@
+"""ctypes binding of libbam.so (include/bam.h).
+
+The CUDA library is the only compute path: importing works without a GPU
+(so CPU-side tests can check the exported symbols), but every compute entry
+point raises if the library is missing or no CUDA device is present.  There
+is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libbam.so")
+
+c_i32, c_i64, c_f32, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
+
+
+class BamBlockSummary(ctypes.Structure):
+    _fields_ = [("or_bits", c_i64), ("and_bits", c_i64), ("lo", c_i64), ("hi", c_i64),
+                ("flags", c_i32), ("pad", c_i32)]
+
+
+class BamAttnFwdParams(ctypes.Structure):
+    _fields_ = [("q", c_vp), ("k", c_vp), ("v", c_vp), ("o", c_vp), ("lse", c_vp),
+                ("desc", c_vp), ("q_gid", c_vp), ("k_row", c_vp), ("row_off", c_vp),
+                ("row_tiles", c_vp), ("order", c_vp),
+                ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
+                ("scale", c_f32)]
+
+
+class BamAttnBwdParams(ctypes.Structure):
+    _fields_ = [("q", c_vp), ("k", c_vp), ("v", c_vp), ("o", c_vp), ("dout", c_vp),
+                ("lse", c_vp), ("delta", c_vp), ("dq_acc", c_vp), ("dq", c_vp), ("dk", c_vp),
+                ("dv", c_vp), ("desc", c_vp), ("q_gid", c_vp), ("k_row", c_vp),
+                ("col_off", c_vp), ("col_tiles", c_vp), ("order", c_vp),
+                ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
+                ("scale", c_f32)]
+
+
+# name -> (restype, argtypes); mirrors include/bam.h exactly
+SIGNATURES = {
+    "bam_last_error": (ctypes.c_char_p, []),
+    "bam_version": (c_i32, []),
+    "bam_mask_expand": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "bam_mask_validate": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
+    "bam_block_summarize": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "bam_classify": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "bam_build_tile_lists": (c_i32, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                     c_vp, c_vp]),
+    "bam_lpt_workspace_bytes": (c_i64, [c_i64]),
+    "bam_lpt_assign": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bam_zigzag_assign": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bam_contiguous_assign": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bam_split_count": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "bam_split_fill": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bam_ilp_optimal": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "bam_attn_fwd": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp]),
+    "bam_attn_bwd": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
+    "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
+    "bam_selftest_umma": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+}
+
+BAM_OK, BAM_INVALID_ARGUMENT, BAM_CUDA_ERROR, BAM_UNSUPPORTED, BAM_BUDGET_EXCEEDED = range(5)
+
+
+class BamError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"libbam error {code}: {message}")
+        self.code = code
+        self.message = message
+
+
+_LIB = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libbam.so (built in-tree by ``__graft_entry__.build()``)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2503_11367_b200 computes on a CUDA device (B200, sm_100a); "
+                           "no CUDA device is visible and there is no CPU fallback")
+
+
+def check(rc: int) -> None:
+    if rc != BAM_OK:
+        msg = load().bam_last_error().decode(errors="replace")
+        raise BamError(rc, msg)
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def call(name: str, *args) -> None:
+    """Call a libbam entry point that ends with a stream argument."""
+    check(getattr(load(), name)(*args, stream()))

@@ -1,0 +1,188 @@
+"""Bitfield-masked attention forward/backward on B200 (libbam tcgen05 kernels).
+
+The reference has no attention code; the semantics are the
+mask predicate of mask.py:106-112 applied to scaled dot-product attention,
+computed blockwise over non-skip 128x128 tiles.
+
+Layouts (token-major, head_dim 128, bf16):
+  q, o, do      [nq*128, Hq, 128]     the local query blocks, local order
+  k, v          [k_rows*128, Hkv, 128] key/value blocks; global block kb sits
+                                       at block-row ``k_row[kb]``
+  lse           [Hq, nq*128] fp32 (natural log)
+GQA: query head h reads KV head h // (Hq // Hkv).
+
+``AttentionPlan`` carries everything derived from the mask and the block
+assignment (classes, W, tile lists, processing orders); it is built once per
+mask on the device and reused by forward and backward.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .mask import BitfieldMask, classify_device
+
+BLOCK = 128
+HEAD_DIM = 128
+
+
+@dataclass
+class AttentionPlan:
+    desc: torch.Tensor        # int64 [nb*128]
+    nb: int
+    classes: torch.Tensor     # uint8 [nb, nb]
+    W: torch.Tensor           # int32 [nb]
+    q_gid: torch.Tensor       # int32 [nq] global block of each local query block
+    k_row: torch.Tensor       # int32 [nb] block-row of global block kb in k/v
+    k_rows: int
+    row_off: torch.Tensor     # int32 [nq+1]
+    row_tiles: torch.Tensor   # int32 kb << 2 | class
+    col_off: torch.Tensor     # int32 [nb+1]
+    col_tiles: torch.Tensor   # int32 j << 2 | class
+    fwd_order: torch.Tensor   # int32 [nq] heavy-first local query blocks
+    bwd_order: torch.Tensor   # int32 [nb] heavy-first key blocks
+
+    @property
+    def nq(self) -> int:
+        return int(self.q_gid.shape[0])
+
+
+def _heavy_first(counts: torch.Tensor) -> torch.Tensor:
+    # stable sort by descending tile count (ties: lower index first)
+    return torch.sort(-counts.to(torch.int64), stable=True).indices.to(torch.int32)
+
+
+def build_plan(desc: torch.Tensor, q_gid: torch.Tensor | None = None,
+               k_row: torch.Tensor | None = None, k_rows: int | None = None,
+               classes: torch.Tensor | None = None, W: torch.Tensor | None = None) -> AttentionPlan:
+    """Plan for query blocks ``q_gid`` (default: all, in order) against all
+    keys at block-rows ``k_row`` (default identity)."""
+    _lib.require_cuda()
+    T = desc.shape[0]
+    if T % BLOCK:
+        raise ValueError(f"attention needs T % {BLOCK} == 0 (T={T})")
+    nb = T // BLOCK
+    dev = desc.device
+    if classes is None:
+        classes, W = classify_device(desc, BLOCK)
+    if q_gid is None:
+        q_gid = torch.arange(nb, dtype=torch.int32, device=dev)
+    if k_row is None:
+        k_row = torch.arange(nb, dtype=torch.int32, device=dev)
+        k_rows = nb
+    nq = int(q_gid.shape[0])
+    row_cnt = torch.empty(nq, dtype=torch.int32, device=dev)
+    row_off = torch.empty(nq + 1, dtype=torch.int32, device=dev)
+    col_cnt = torch.empty(nb, dtype=torch.int32, device=dev)
+    col_off = torch.empty(nb + 1, dtype=torch.int32, device=dev)
+    _lib.call("bam_build_tile_lists", classes.data_ptr(), nb, q_gid.data_ptr(), nq,
+              row_cnt.data_ptr(), row_off.data_ptr(), None, col_cnt.data_ptr(), col_off.data_ptr(),
+              None)
+    n_row = int(row_off[-1].item())
+    n_col = int(col_off[-1].item())
+    row_tiles = torch.empty(max(n_row, 1), dtype=torch.int32, device=dev)
+    col_tiles = torch.empty(max(n_col, 1), dtype=torch.int32, device=dev)
+    _lib.call("bam_build_tile_lists", classes.data_ptr(), nb, q_gid.data_ptr(), nq,
+              row_cnt.data_ptr(), row_off.data_ptr(), row_tiles.data_ptr(), col_cnt.data_ptr(),
+              col_off.data_ptr(), col_tiles.data_ptr())
+    return AttentionPlan(desc=desc, nb=nb, classes=classes, W=W, q_gid=q_gid.to(torch.int32),
+                         k_row=k_row.to(torch.int32), k_rows=int(k_rows), row_off=row_off,
+                         row_tiles=row_tiles, col_off=col_off, col_tiles=col_tiles,
+                         fwd_order=_heavy_first(row_cnt), bwd_order=_heavy_first(col_cnt))
+
+
+def plan_for_mask(mask: BitfieldMask) -> AttentionPlan:
+    return build_plan(mask.device_descriptors())
+
+
+def _check_qkv(q, k, v, plan: AttentionPlan):
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor")
+        if t.dim() != 3 or t.shape[2] != HEAD_DIM:
+            raise ValueError(f"{name} must be [tokens, heads, {HEAD_DIM}]")
+    if q.shape[0] != plan.nq * BLOCK:
+        raise ValueError(f"q has {q.shape[0]} rows, plan expects {plan.nq * BLOCK}")
+    if k.shape != v.shape or k.shape[0] != plan.k_rows * BLOCK:
+        raise ValueError(f"k/v must be [{plan.k_rows * BLOCK}, Hkv, {HEAD_DIM}]")
+    if q.shape[1] % k.shape[1]:
+        raise ValueError("Hq must be a multiple of Hkv")
+
+
+def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None):
+    """Returns (o bf16 [nq*128, Hq, 128], lse fp32 [Hq, nq*128])."""
+    _check_qkv(q, k, v, plan)
+    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+    Hq, Hkv = q.shape[1], k.shape[1]
+    o = torch.empty_like(q)
+    lse = torch.empty(Hq, q.shape[0], dtype=torch.float32, device=q.device)
+    p = _lib.BamAttnFwdParams(
+        q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
+        plan.desc.data_ptr(), plan.q_gid.data_ptr(), plan.k_row.data_ptr(),
+        plan.row_off.data_ptr(), plan.row_tiles.data_ptr(), plan.fwd_order.data_ptr(),
+        plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale)
+    _lib.check(_lib.load().bam_attn_fwd(p, _lib.stream()))
+    return o, lse
+
+
+def attn_backward(q, k, v, o, lse, do, plan: AttentionPlan, scale: float | None = None,
+                  dkv_fp32: bool = False):
+    """Returns (dq bf16, dk, dv) with dk/dv fp32 [k_rows*128, Hkv, 128]
+    partials when ``dkv_fp32`` (for a CP reduce-scatter), else bf16."""
+    _check_qkv(q, k, v, plan)
+    for name, t in (("o", o), ("do", do)):
+        if t.shape != q.shape or t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous bf16 tensor shaped like q")
+    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+    Hq, Hkv = q.shape[1], k.shape[1]
+    dev = q.device
+    delta = torch.empty(Hq, q.shape[0], dtype=torch.float32, device=dev)
+    dq_acc = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    dq = torch.empty_like(q)
+    dk = torch.empty(k.shape, dtype=torch.float32, device=dev)
+    dv = torch.empty(k.shape, dtype=torch.float32, device=dev)
+    p = _lib.BamAttnBwdParams(
+        q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(),
+        delta.data_ptr(), dq_acc.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+        plan.desc.data_ptr(), plan.q_gid.data_ptr(), plan.k_row.data_ptr(),
+        plan.col_off.data_ptr(), plan.col_tiles.data_ptr(), plan.bwd_order.data_ptr(),
+        plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale)
+    _lib.check(_lib.load().bam_attn_bwd(p, _lib.stream()))
+    if dkv_fp32:
+        return dq, dk, dv
+    return dq, to_bf16(dk), to_bf16(dv)
+
+
+def to_bf16(x: torch.Tensor) -> torch.Tensor:
+    out = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+    _lib.call("bam_f32_to_bf16", x.data_ptr(), out.data_ptr(), x.numel())
+    return out
+
+
+class _BitfieldAttention(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, plan, scale):
+        o, lse = attn_forward(q, k, v, plan, scale)
+        ctx.save_for_backward(q, k, v, o, lse)
+        ctx.plan = plan
+        ctx.scale = scale
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse = ctx.saved_tensors
+        dq, dk, dv = attn_backward(q, k, v, o, lse, do.contiguous(), ctx.plan, ctx.scale)
+        return dq, dk, dv, None, None
+
+
+def bitfield_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                       mask_or_plan, scale: float | None = None) -> torch.Tensor:
+    """Single-GPU bitfield-masked attention with autograd.
+
+    ``mask_or_plan``: a ``BitfieldMask`` (planned here) or an ``AttentionPlan``."""
+    plan = mask_or_plan if isinstance(mask_or_plan, AttentionPlan) else plan_for_mask(mask_or_plan)
+    return _BitfieldAttention.apply(q, k, v, plan, scale)

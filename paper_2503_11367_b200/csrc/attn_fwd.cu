@@ -1,0 +1,268 @@
+// Bitfield-masked attention forward for sm_100a (tcgen05 + TMEM + TMA).
+//
+// Semantics: O = softmax(scale * Q K^T, masked by materialize()) V per query
+// head, mask per reference mask.py:106-112, computed blockwise over the
+// non-skip 128x128 tiles only: FULL tiles take no mask,
+// PARTIAL tiles evaluate the 64-bit descriptor predicate in registers.
+//
+// One CTA = one 128-row query block x one query head; 2 CTAs per SM so one
+// CTA's softmax overlaps the other's MMAs.
+//   warps 0-3  softmax: thread r owns row r (= TMEM lane r); online softmax
+//              with lazy (2^8) rescaling of the TMEM O accumulator
+//   warp 4     TMA producer: Q once, then K / V tiles (single-buffered each;
+//              K(t+1) streams in during softmax(t), V(t+1) during S(t+1))
+//   warp 5     TMEM allocator + MMA issuer (one thread):
+//              S = Q K^T (SS, K-major x K-major) -> TMEM cols [0,128)
+//              O += P V  (TS: P bf16 in TMEM cols [0,64), V MN-major) -> [128,256)
+#include "../../include/bam.h"
+#include "common.cuh"
+#include "tma.h"
+
+namespace bam {
+
+namespace fwd {
+
+constexpr int kThreads = 192;
+constexpr uint32_t kTileBytes = 128 * 128 * 2;  // one 128x128 bf16 tile (two 64-col boxes)
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kColS = 0, kColO = 128;
+
+struct Smem {
+  alignas(1024) uint8_t q[kTileBytes];
+  alignas(1024) uint8_t k[kTileBytes];
+  alignas(1024) uint8_t v[kTileBytes];
+  uint64_t bar_q, bar_k_full, bar_k_empty, bar_v_full, bar_v_empty;
+  uint64_t bar_s_full, bar_p_full, bar_pv_done;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void load_tile(const CUtensorMap* m, uint64_t* bar, uint8_t* dst,
+                                          int head, int row0) {
+  tma_load_3d(m, bar, dst, 0, head, row0);
+  tma_load_3d(m, bar, dst + kTileBytes / 2, 64, head, row0);
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int h = blockIdx.x;
+  const int j = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
+  const int hkv = h / (p.Hq / p.Hkv);
+  const int t0 = p.row_off[j], n = p.row_off[j + 1] - t0;
+  const int32_t* tiles = p.row_tiles + t0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar_q, 1);
+    mbar_init(&sm.bar_k_full, 1);
+    mbar_init(&sm.bar_k_empty, 1);
+    mbar_init(&sm.bar_v_full, 1);
+    mbar_init(&sm.bar_v_empty, 1);
+    mbar_init(&sm.bar_s_full, 1);
+    mbar_init(&sm.bar_p_full, 128);
+    mbar_init(&sm.bar_pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) {
+    tmem_alloc(&sm.tmem_base, kTmemCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && n > 0) {
+      prefetch_tmap(&tm_q);
+      prefetch_tmap(&tm_k);
+      prefetch_tmap(&tm_v);
+      mbar_expect_tx(&sm.bar_q, kTileBytes);
+      load_tile(&tm_q, &sm.bar_q, sm.q, h, j * 128);
+      for (int t = 0; t < n; ++t) {
+        const int krow = p.k_row[tiles[t] >> 2] * 128;
+        if (t > 0) mbar_wait(&sm.bar_k_empty, (t - 1) & 1);
+        mbar_expect_tx(&sm.bar_k_full, kTileBytes);
+        load_tile(&tm_k, &sm.bar_k_full, sm.k, hkv, krow);
+        if (t > 0) mbar_wait(&sm.bar_v_empty, (t - 1) & 1);
+        mbar_expect_tx(&sm.bar_v_full, kTileBytes);
+        load_tile(&tm_v, &sm.bar_v_full, sm.v, hkv, krow);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && n > 0) {
+      const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      const uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
+      const uint32_t sq = smem_u32(sm.q), sk = smem_u32(sm.k), sv = smem_u32(sm.v);
+      mbar_wait(&sm.bar_q, 0);
+      for (int t = 0; t < n; ++t) {
+        mbar_wait(&sm.bar_k_full, t & 1);
+        if (t > 0) mbar_wait(&sm.bar_pv_done, (t - 1) & 1);  // P(t-1) in S cols consumed
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
+          mma_ss(tmem + kColS, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024),
+                 idesc_s, kk > 0);
+        }
+        tc_commit(&sm.bar_s_full);
+        tc_commit(&sm.bar_k_empty);
+        mbar_wait(&sm.bar_p_full, t & 1);
+        mbar_wait(&sm.bar_v_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + kColO, tmem + kColS + kk * 8,
+                 sdesc_sw128(sv + kk * 2048, kTileBytes / 2, 1024), idesc_o, (t > 0 || kk > 0));
+        tc_commit(&sm.bar_pv_done);
+        tc_commit(&sm.bar_v_empty);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps 0-3
+    const int r = warp * 32 + lane;
+    const uint32_t lane_base = (warp * 32) << 16;
+    const long long qg = (long long)p.q_gid[j] * 128 + r;
+    const long long dq = p.desc[qg];
+    const float scale_log2 = p.scale * 1.4426950408889634f;
+    float m = -INFINITY, l = 0.f;
+    for (int t = 0; t < n; ++t) {
+      const int e = tiles[t];
+      const int cls = e & 3;
+      const long long kg0 = (long long)(e >> 2) * 128;
+      mbar_wait(&sm.bar_s_full, t & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rr[32];
+        BAM_TMEM_LD32(tmem + lane_base + kColS + c * 32, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(rr[i]);
+      }
+      if (cls == 2) {  // PARTIAL: descriptor predicate per element, 32 columns at a time
+        const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t bits = 0;
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i) {
+            const long long d = __ldg(dk + c * 32 + i);
+            bits |= uint32_t(bam_allowed(dq, qg, d, kg0 + c * 32 + i)) << i;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (!((bits >> i) & 1)) s[c * 32 + i] = -INFINITY;
+        }
+      }
+      float mt = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) mt = fmaxf(mt, s[c]);
+      const float m_new = fmaxf(m, mt * scale_log2);
+      // lazy rescale: only when the running max grows by more than 2^8
+      const bool rescale = m_new > m + 8.f;
+      const float alpha = rescale ? ex2(m - m_new) : 1.f;  // m = -inf -> 0
+      if (rescale) {
+        l *= alpha;
+        m = m_new;
+      }
+      const float mb = (m == -INFINITY) ? 0.f : m;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2(fmaf(s[c * 32 + 2 * i], scale_log2, -mb));
+          const float p1 = ex2(fmaf(s[c * 32 + 2 * i + 1], scale_log2, -mb));
+          l += p0 + p1;
+          pk[i] = pack_bf16(p0, p1);
+        }
+        BAM_TMEM_ST16(tmem + lane_base + kColS + c * 16, pk);
+      }
+      if (rescale && t > 0) {  // O(t-1) is complete: S(t) was issued after PV(t-1) retired
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t rr[32];
+          BAM_TMEM_LD32(tmem + lane_base + kColO + c * 32, rr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+          BAM_TMEM_ST32(tmem + lane_base + kColO + c * 32, rr);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm.bar_p_full);
+    }
+    // epilogue: O / l -> bf16, LSE
+    const int64_t Tq = (int64_t)p.nq * 128;
+    const int64_t row = (int64_t)j * 128 + r;
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + (row * p.Hq + h) * 128;
+    if (n > 0) {
+      mbar_wait(&sm.bar_pv_done, (n - 1) & 1);
+      tc_fence_after();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rr[32];
+        BAM_TMEM_LD32(tmem + lane_base + kColO + c * 32, rr);
+        tmem_wait_ld();
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(rr[8 * i + 0]) * inv, __uint_as_float(rr[8 * i + 1]) * inv);
+          v.y = pack_bf16(__uint_as_float(rr[8 * i + 2]) * inv, __uint_as_float(rr[8 * i + 3]) * inv);
+          v.z = pack_bf16(__uint_as_float(rr[8 * i + 4]) * inv, __uint_as_float(rr[8 * i + 5]) * inv);
+          v.w = pack_bf16(__uint_as_float(rr[8 * i + 6]) * inv, __uint_as_float(rr[8 * i + 7]) * inv);
+          dst[i] = v;
+        }
+      }
+      p.lse[(int64_t)h * Tq + row] =
+          l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    } else {
+      uint4* dst = reinterpret_cast<uint4*>(orow);
+      for (int i = 0; i < 16; ++i) dst[i] = make_uint4(0, 0, 0, 0);
+      p.lse[(int64_t)h * Tq + row] = -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+}  // namespace fwd
+}  // namespace bam
+
+using namespace bam;
+
+extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
+  BAM_CHECK_ARG(pp != nullptr, "bam_attn_fwd: null params");
+  const BamAttnFwdParams& p = *pp;
+  BAM_CHECK_ARG(p.nq >= 1 && p.nb >= 1 && p.k_rows >= 1, "bam_attn_fwd: nq=%d nb=%d k_rows=%d",
+                p.nq, p.nb, p.k_rows);
+  BAM_CHECK_ARG(p.Hq >= 1 && p.Hkv >= 1 && p.Hq % p.Hkv == 0,
+                "bam_attn_fwd: Hq=%d must be a multiple of Hkv=%d", p.Hq, p.Hkv);
+  BAM_CHECK_ARG(p.nq <= 65535, "bam_attn_fwd: nq=%d > 65535", p.nq);
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  const int smem = (int)sizeof(fwd::Smem) + 1024;
+  BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid(p.Hq, p.nq);
+  fwd::attn_fwd_kernel<<<grid, fwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, p);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}

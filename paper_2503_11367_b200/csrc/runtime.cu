@@ -1,0 +1,153 @@
+// Host-side runtime of libbam: error reporting, the exact ILP oracle of the
+// reference API (balance.py:124-192, host C++), fp32->bf16 conversion and the
+// tcgen05/TMA self test.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <set>
+#include <vector>
+
+#include "../../include/bam.h"
+#include "common.cuh"
+#include "tma.h"
+
+namespace bam {
+
+static thread_local char g_last_error[1024] = "";
+
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+// ----------------------------------------------------------------------------- ILP (host)
+// balance.py:106-121 (_feasible): can `jobs` be packed with every load <= limit?
+static bool feasible(const int64_t* jobs, int n, std::vector<int64_t>& loads, int64_t limit) {
+  if (n == 0) return true;
+  std::set<int64_t> tried;  // identical loads are symmetric
+  for (size_t g = 0; g < loads.size(); ++g) {
+    if (!tried.insert(loads[g]).second) continue;
+    if (loads[g] + jobs[0] <= limit) {
+      loads[g] += jobs[0];
+      const bool ok = feasible(jobs + 1, n - 1, loads, limit);
+      loads[g] -= jobs[0];
+      if (ok) return true;
+    }
+  }
+  return false;
+}
+
+struct Search {
+  std::vector<int64_t> jobs;
+  int64_t best, lower;
+  int G;
+  void run(size_t idx, std::vector<int64_t>& loads) {  // balance.py:148-163
+    if (best == lower) return;
+    if (idx == jobs.size()) {
+      best = std::min(best, *std::max_element(loads.begin(), loads.end()));
+      return;
+    }
+    std::set<int64_t> tried;
+    for (int g = 0; g < G; ++g) {
+      if (!tried.insert(loads[g]).second) continue;
+      if (loads[g] + jobs[idx] >= best) continue;
+      loads[g] += jobs[idx];
+      run(idx + 1, loads);
+      loads[g] -= jobs[idx];
+    }
+  }
+};
+
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ src, uint2* __restrict__ dst,
+                                   int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = src[i];
+    dst[i] = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+  }
+}
+
+}  // namespace bam
+
+using namespace bam;
+
+extern "C" {
+
+const char* bam_last_error(void) { return g_last_error; }
+int bam_version(void) { return 1; }
+
+int bam_ilp_optimal(const int64_t* w, int32_t n, int32_t G, int32_t* assignment,
+                    int64_t* makespan) {
+  if (n < 1) {
+    set_last_error("workloads must be nonempty");
+    return BAM_INVALID_ARGUMENT;
+  }
+  if (n > 14 || G > 4) {
+    set_last_error("instance (%d blocks, %d GPUs) exceeds the exact-search budget (14 blocks, 4 GPUs)",
+                   n, G);
+    return BAM_BUDGET_EXCEEDED;
+  }
+  if (G < 1) {
+    set_last_error("num_gpus must be >= 1");
+    return BAM_INVALID_ARGUMENT;
+  }
+  Search s;
+  s.G = G;
+  s.jobs.assign(w, w + n);
+  std::stable_sort(s.jobs.begin(), s.jobs.end(), [](int64_t a, int64_t b) { return a > b; });
+  int64_t total = 0;
+  for (int64_t j : s.jobs) total += j;
+  s.lower = std::max(s.jobs[0], (total + G - 1) / G);
+  s.best = total;
+  std::vector<int64_t> loads(G, 0);
+  s.run(0, loads);
+  const int64_t opt = s.best;
+  // lexicographic extraction (balance.py:169-189)
+  std::vector<int> by_size(n);
+  for (int i = 0; i < n; ++i) by_size[i] = i;
+  std::stable_sort(by_size.begin(), by_size.end(), [&](int a, int b) { return w[a] > w[b]; });
+  std::vector<int> asg(n, -1);
+  std::fill(loads.begin(), loads.end(), 0);
+  for (int b = 0; b < n; ++b) {
+    bool placed = false;
+    for (int g = 0; g < G && !placed; ++g) {
+      if (loads[g] + w[b] > opt) continue;
+      loads[g] += w[b];
+      asg[b] = g;
+      std::vector<int64_t> rem;
+      for (int j : by_size)
+        if (asg[j] == -1) rem.push_back(w[j]);
+      if (feasible(rem.data(), (int)rem.size(), loads, opt)) {
+        placed = true;
+      } else {
+        loads[g] -= w[b];
+        asg[b] = -1;
+      }
+    }
+    if (!placed) {
+      set_last_error("internal error: optimal makespan not extractable");
+      return BAM_INVALID_ARGUMENT;
+    }
+  }
+  for (int b = 0; b < n; ++b) assignment[b] = asg[b];
+  *makespan = opt;
+  return BAM_OK;
+}
+
+int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
+  BAM_CHECK_ARG(n % 4 == 0, "bam_f32_to_bf16: n=%lld must be a multiple of 4", (long long)n);
+  const int64_t n4 = n / 4;
+  if (n4 == 0) return kOk;
+  int64_t grid = (n4 + 255) / 256;
+  if (grid > 148 * 32) grid = 148 * 32;
+  f32_to_bf16_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<uint2*>(dst), n4);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+}  // extern "C"

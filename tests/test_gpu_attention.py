@@ -1,0 +1,144 @@
+"""GPU parity: tcgen05 attention forward/backward vs the fp32 CPU oracle.
+
+Tolerance (BASELINE.json north star): bf16 kernel vs fp32 oracle,
+max-abs <= 2e-2 and relative-L2 <= 1e-2 on O, dQ, dK, dV; LSE max-abs 2e-3.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention_ref, mask_ref
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-2
+REL_L2 = 1e-2
+
+
+def rel_l2(a, b):
+    a, b = a.float().cpu(), b.float().cpu()
+    return ((a - b).norm() / b.norm().clamp_min(1e-12)).item()
+
+
+def max_abs(a, b):
+    return (a.float().cpu() - b.float().cpu()).abs().max().item()
+
+
+def inputs(T, Hq, Hkv, seed=1234):
+    g = torch.Generator().manual_seed(seed)
+    q = torch.randn(T, Hq, 128, generator=g).to(torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, generator=g).to(torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, generator=g).to(torch.bfloat16)
+    do = torch.randn(T, Hq, 128, generator=g).to(torch.bfloat16)
+    return q, k, v, do
+
+
+def assert_close(name, got, ref):
+    ma, rl = max_abs(got, ref), rel_l2(got, ref)
+    assert ma <= MAX_ABS and rl <= REL_L2, f"{name}: max-abs {ma:.3e} rel-L2 {rl:.3e}"
+
+
+def run_case(desc_list, Hq, Hkv, seed=1234, check_bwd=True):
+    from paper_2503_11367_b200 import attention as A
+
+    desc = np.asarray(desc_list, dtype=np.int64)
+    T = desc.shape[0]
+    q, k, v, do = inputs(T, Hq, Hkv, seed)
+    dev = torch.device("cuda")
+    plan = A.build_plan(torch.from_numpy(desc).to(dev))
+    # plan tile lists must equal the oracle's classification
+    ref_cls, ref_w = mask_ref.block_workloads_np(desc, 128)
+    assert np.array_equal(plan.classes.cpu().numpy(), ref_cls)
+    assert np.array_equal(plan.W.cpu().numpy(), ref_w)
+    qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
+    o, lse = A.attn_forward(qd, kd, vd, plan)
+    torch.cuda.synchronize()
+    pos = np.arange(T)
+    o_ref, lse_ref = attention_ref.attention_fwd(q, k, v, desc, pos)
+    assert_close("O", o, o_ref)
+    assert max_abs(lse, lse_ref) <= 2e-3, f"LSE max-abs {max_abs(lse, lse_ref):.3e}"
+    if not check_bwd:
+        return
+    dq, dk, dv = A.attn_backward(qd, kd, vd, o, lse, dod, plan, dkv_fp32=True)
+    torch.cuda.synchronize()
+    dq_ref, dk_ref, dv_ref = attention_ref.attention_bwd(q, k, v, o_ref, lse_ref, do, desc, pos)
+    assert_close("dQ", dq, dq_ref)
+    assert_close("dK", dk, dk_ref)
+    assert_close("dV", dv, dv_ref)
+
+
+def test_selftest_umma():
+    from paper_2503_11367_b200 import _lib
+
+    g = torch.Generator().manual_seed(7)
+    a, b, v, x = (torch.randn(128, 128, generator=g).to(torch.bfloat16) for _ in range(4))
+    dev = torch.device("cuda")
+    out = torch.empty(3, 128, 128, dtype=torch.float32, device=dev)
+    ad, bd, vd, xd = (t.to(dev) for t in (a, b, v, x))
+    _lib.call("bam_selftest_umma", ad.data_ptr(), bd.data_ptr(), vd.data_ptr(), xd.data_ptr(),
+              out.data_ptr())
+    torch.cuda.synchronize()
+    out = out.cpu()
+    af, bf, vf, xf = (t.float() for t in (a, b, v, x))
+    for i, ref in enumerate((af @ bf.t(), af @ vf, xf.t() @ vf)):
+        err = (out[i] - ref).abs().max().item()
+        assert err < 1e-2, f"selftest mode {i}: max err {err}"
+
+
+def test_text_image_small():
+    desc, _ = mask_ref.build_bitfield([("text", 128), ("image", 256), ("text", 384)])
+    run_case(desc, 4, 2)
+
+
+def test_causal_small_gqa():
+    desc, _ = mask_ref.build_bitfield([("text", 1024)])
+    run_case(desc, 8, 2)
+
+
+def test_multimodal_partial_tiles():
+    # non-aligned segments: many PARTIAL tiles, segments split across blocks
+    desc, _ = mask_ref.build_bitfield([("text", 100), ("vision", 300), ("text", 77),
+                                       ("audio", 211), ("text", 120), ("vision", 88),
+                                       ("text", 128)])
+    run_case(desc, 2, 2)
+
+
+def test_raw_descriptors():
+    rng = np.random.default_rng(5)
+    T = 768
+    desc = []
+    while len(desc) < T:
+        run = int(rng.integers(1, 90))
+        if rng.random() < 0.5:
+            d = 1 | int(sum(2 << j for j in range(3) if rng.random() < 0.5))
+        else:
+            d = 2 << int(rng.integers(0, 3))
+        desc += [d] * min(run, T - len(desc))
+    run_case(desc, 2, 1)
+
+
+def test_config1_full():
+    # BASELINE.json config 1: 1 image + text, 4K, 8 heads
+    desc, _ = mask_ref.build_bitfield([("text", 128), ("image", 1024), ("text", 2944)])
+    run_case(desc, 8, 8)
+
+
+def test_autograd_function():
+    from paper_2503_11367_b200 import attention as A
+    from paper_2503_11367_b200 import mask as M
+
+    mask = M.build_bitfield([("text", 256), ("image", 256), ("text", 256)])
+    q, k, v, do = inputs(768, 4, 4, seed=3)
+    dev = torch.device("cuda")
+    qd, kd, vd = (t.to(dev).requires_grad_(True) for t in (q, k, v))
+    o = A.bitfield_attention(qd, kd, vd, mask)
+    o.backward(do.to(dev))
+    desc = np.asarray(mask.descriptors, dtype=np.int64)
+    o_ref, q_g, k_g, v_g = attention_ref.attention_dense_autograd(q, k, v, do, desc, np.arange(768))
+    assert_close("O", o.detach(), o_ref)
+    assert_close("dQ", qd.grad, q_g)
+    assert_close("dK", kd.grad, k_g)
+    assert_close("dV", vd.grad, v_g)
