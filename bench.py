@@ -1,0 +1,371 @@
+#!/usr/bin/env python3
+"""Benchmark: bitfield-masked attention fwd+bwd (CP over N GPUs) on B200.
+
+Metric (BASELINE.json): masked-attn fwd+bwd TFLOP/s and % of dense BF16 peak
+at CP = 1/2/4/8, with the per-rank load imbalance.  A step is one forward +
+backward of the context-parallel attention over the whole sequence of the
+workload (default: config 4, the 128K EMU-style interleaved multi-image mask,
+GQA 32q/8kv, d=128), including the K/V all-gather and the dK/dV
+reduce-scatter when N > 1.  The sequence is fixed as N grows ("strong").
+
+Algorithmic FLOP per step = 14 * d * Hq * N_allowed (fwd 4, bwd 10; the
+FlashAttention convention), N_allowed = exact count of mask.py:106-112 true
+pairs (bam_count_allowed, no tile padding).  value = FLOP / max-over-ranks
+step time (whole job); tflops_per_gpu = value / N.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+        python bench.py --impl reference ...    (the CPU path, see below)
+
+--impl reference times the reference's CPU implementation of the path: the
+reference itself is pure Python with no attention code, so the
+arm runs the repo's CPU oracle port (oracle/: fp32 masked attention on all
+host threads, plus the C restatement of block_workloads), on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D = 128
+PEAKS_FALLBACK = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
+METRIC = "masked-attn fwd+bwd TFLOP/s/GPU & %BF16 peak at CP=1/2/4/8; load imbalance"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return p, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="bam", choices=["bam", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--policy", default="lpt", choices=["lpt", "zigzag", "contiguous"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-blocks", type=int, default=2)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": rows[0][1],
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- CPU arm
+def cpu_attention_sample(segments, Hq, Hkv, blocks, seed=1234):
+    """fp32 oracle fwd+bwd for `blocks` query blocks (all heads) against all
+    keys; returns (seconds, masked FLOP, sample description)."""
+    import numpy as np
+    import torch
+
+    from oracle import attention_ref, mask_ref
+
+    desc, _ = mask_ref.build_bitfield(segments)
+    desc = np.asarray(desc, np.int64)
+    T = desc.shape[0]
+    g = torch.Generator().manual_seed(seed)
+    k = torch.randn(T, Hkv, D, generator=g)
+    v = torch.randn(T, Hkv, D, generator=g)
+    rows = np.concatenate([np.arange(b * 128, (b + 1) * 128) for b in blocks])
+    q = torch.randn(len(rows), Hq, D, generator=g)
+    do = torch.randn(len(rows), Hq, D, generator=g)
+    n_allowed = mask_ref.count_allowed_rows(desc, rows)
+    t0 = time.perf_counter()
+    o, lse = attention_ref.attention_fwd(q, k, v, desc, rows)
+    attention_ref.attention_bwd(q, k, v, o, lse, do, desc, rows)
+    dt = time.perf_counter() - t0
+    return dt, 14.0 * D * Hq * n_allowed, f"{len(blocks)} query block(s) {list(blocks)} x {Hq} heads vs all {T} keys"
+
+
+def sample_blocks(nb, count, step=0):
+    return [int((i + 0.5 + step * 0.37) * nb / count) % nb for i in range(count)]
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU path timed on the host cores (rank 0 only)."""
+    import torch
+
+    if rank != 0:
+        return
+    threads = torch.get_num_threads()
+    nb = sum(c for _, c in cfg["segments"]) // 128
+    for w in range(args.warmup):
+        cpu_attention_sample(cfg["segments"], cfg["Hq"], cfg["Hkv"], sample_blocks(nb, 1, w))
+    times, flops = [], []
+    for s in range(args.steps):
+        dt, fl, sample = cpu_attention_sample(cfg["segments"], cfg["Hq"], cfg["Hkv"],
+                                              sample_blocks(nb, 1, s + args.warmup))
+        times.append(dt)
+        flops.append(fl)
+    value = sum(flops) / sum(times) / 1e12
+    ms = 1e3 * sum(times) / len(times)
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg["name"], "tokens": nb * 128, "Hq": cfg["Hq"],
+                   "Hkv": cfg["Hkv"], "head_dim": D, "cp": world},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                         "sample": "per step: 1 query block x all heads vs all keys, fp32 "
+                                   "oracle fwd+bwd (oracle/attention_ref.py; the reference "
+                                   "has no attention code)"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2503_11367_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2503_11367_b200 import _lib, attention as A, cp as CP, mask as M
+
+    Hq, Hkv = cfg["Hq"], cfg["Hkv"]
+    mask = M.build_bitfield(cfg["segments"])
+    desc = mask.device_descriptors()
+    T = desc.shape[0]
+    n_allowed = M.count_allowed(desc)
+    flop_step = 14.0 * D * Hq * n_allowed
+
+    plan = CP.make_cp_plan(desc, world, rank, args.policy)
+    layout = plan.layout
+    loads = plan.assignment.loads.cpu().tolist()
+    imb_pred = max(loads) / (sum(loads) / len(loads)) if sum(loads) else 1.0
+
+    # synthetic inputs: same bytes on every rank (cuda generator, seed 1234, order Q K V dO)
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    q = torch.randn(T, Hq, D, device=dev, generator=gen, dtype=torch.bfloat16)
+    k = torch.randn(T, Hkv, D, device=dev, generator=gen, dtype=torch.bfloat16)
+    v = torch.randn(T, Hkv, D, device=dev, generator=gen, dtype=torch.bfloat16)
+    do = torch.randn(T, Hq, D, device=dev, generator=gen, dtype=torch.bfloat16)
+    q_loc, k_loc, v_loc, do_loc = (CP.shard_rows(t, layout).contiguous() for t in (q, k, v, do))
+    del q, k, v, do
+    # local share of the algorithmic FLOP (for the per-kernel roofline)
+    rows_allowed = None
+    flop_local_fwd = 4.0 * D * Hq * n_allowed / world
+    flop_local_bwd = 10.0 * D * Hq * n_allowed / world
+
+    def step(ev):
+        if world > 1:
+            k_all, v_all = CP.gather_kv(k_loc, v_loc, layout)
+        else:
+            k_all, v_all = k_loc, v_loc
+        ev[0].record()
+        o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn)
+        ev[1].record()
+        dq, dk_all, dv_all = A.attn_backward(q_loc, k_all, v_all, o, lse, do_loc, plan.attn,
+                                             dkv_fp32=True, timer=(ev[2], ev[3]))
+        ev[4].record()
+        if world > 1:
+            dk, dv = CP.scatter_dkv(dk_all, dv_all, layout)
+        else:
+            dk, dv = dk_all, dv_all
+        dk, dv = A.to_bf16(dk.contiguous()), A.to_bf16(dv.contiguous())
+        return dq, dk, dv
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(5)]  # noqa: E731
+    for _ in range(args.warmup):
+        step(mk())
+    barrier()
+    evs = [mk() for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.launch_count
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        start.record()
+        for s in range(args.steps):
+            step(evs[s])
+        end.record()
+        barrier()
+    launches = _lib.launch_count - launches0
+    elapsed = start.elapsed_time(end)
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    bwd_main_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    bwd_ms = sum(e[1].elapsed_time(e[4]) for e in evs) / args.steps
+    compute_ms = fwd_ms + bwd_ms
+    t = torch.tensor([elapsed, compute_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        elapsed_max = tmax[0].item()
+        imb_meas = tmax[1].item() / (tsum[1].item() / world)
+    else:
+        elapsed_max = elapsed
+        imb_meas = 1.0
+    ms_step = elapsed_max / args.steps
+    value = flop_step / (ms_step * 1e-3) / 1e12
+
+    # ---------------------------------------------------------------- e2e (public API, host buffers)
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3))
+    h_in = [t.cpu().pin_memory() for t in (q_loc, k_loc, v_loc, do_loc)]
+    h_out = [torch.empty(t.shape, dtype=torch.bfloat16).pin_memory()
+             for t in (q_loc, q_loc, k_loc, v_loc)]
+    h2d = sum(t.numel() * t.element_size() for t in h_in)
+    d2h = sum(t.numel() * t.element_size() for t in h_out)
+
+    def e2e_step():
+        qd, kd, vd, dod = (t.to(dev, non_blocking=True) for t in h_in)
+        qd.requires_grad_(True)
+        kd.requires_grad_(True)
+        vd.requires_grad_(True)
+        if world > 1:
+            o = CP.cp_bitfield_attention(qd, kd, vd, plan)
+        else:
+            o = A.bitfield_attention(qd, kd, vd, plan.attn)
+        o.backward(dod)
+        for dst, src in zip(h_out, (o.detach(), qd.grad, kd.grad, vd.grad)):
+            dst.copy_(src, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+    e2e_value = flop_step / (e2e_ms * 1e-3) / 1e12
+
+    peaks, peak_src = load_peaks()
+    peak = peaks["bf16_tflops"]
+    bwd_achieved = flop_local_bwd / (bwd_main_ms * 1e-3) / 1e12
+    fwd_achieved = flop_local_fwd / (fwd_ms * 1e-3) / 1e12
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import torch as _t
+        nb = T // 128
+        dt, fl, sample = cpu_attention_sample(cfg["segments"], Hq, Hkv,
+                                              sample_blocks(nb, args.cpu_sample_blocks))
+        cpu_baseline = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": _t.get_num_threads(),
+                        "kind": "port", "sample": sample + " (fp32 oracle fwd+bwd, torch CPU)",
+                        "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": cfg["name"], "tokens": T, "Hq": Hq, "Hkv": Hkv, "head_dim": D,
+                       "cp": world, "policy": args.policy, "n_allowed": n_allowed,
+                       "flop_per_step": flop_step,
+                       "l2": "inputs larger than L2 (Q alone %.2f GiB per rank)" %
+                             (q_loc.numel() * 2 / 2**30)},
+            "tflops_per_gpu": value / world,
+            "frac_of_peak": value / world / peak,
+            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "bwd_main_ms": bwd_main_ms,
+            "imbalance_predicted": imb_pred, "imbalance_measured": imb_meas,
+            "roofline": {"bound": "tensor", "kernel": "bam attn_bwd_kernel (tcgen05)",
+                         "achieved": bwd_achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": bwd_achieved / peak, "traffic": None,
+                         "peak_source": peak_src + " bf16_tflops (burst)",
+                         "fwd": {"kernel": "bam attn_fwd_kernel", "achieved": fwd_achieved,
+                                 "frac": fwd_achieved / peak}},
+            "cpu_baseline": cpu_baseline,
+            "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                    "api": "cp_bitfield_attention" if world > 1 else "bitfield_attention"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

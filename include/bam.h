@@ -75,6 +75,12 @@ int bam_block_summarize(const int64_t* desc, int64_t T, int64_t block_size,
 int bam_classify(const int64_t* desc, const BamBlockSummary* summaries, int64_t nb,
                  uint8_t* classes, int32_t* W, void* stream);
 
+/* Exact count of allowed (q, k) pairs (materialize() true) given classes:
+ * the algorithmic-FLOP basis of the attention (4*d*Hq per pair forward,
+ * 10*d*Hq backward).  out: device u64. */
+int bam_count_allowed(const int64_t* desc, const BamBlockSummary* summaries,
+                      const uint8_t* classes, int64_t nb, unsigned long long* out, void* stream);
+
 /* Tile lists for the attention kernels over the local query blocks q_gid[nq]:
  * CSR rows (entry kb << 2 | class, kb ascending) and CSC columns over all nb
  * key blocks (entry j << 2 | class, j = local q index ascending).
@@ -167,6 +173,12 @@ typedef struct BamAttnBwdParams {
   float scale;
 } BamAttnBwdParams;
 int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
+/* The three launches bam_attn_bwd performs, exposed for per-kernel timing:
+ * preprocess (delta = rowsum(dO*O), zero dq_acc), main (the tcgen05 kernel),
+ * finalize (dq = scale * dq_acc -> bf16). */
+int bam_attn_bwd_preprocess(const BamAttnBwdParams* p, void* stream);
+int bam_attn_bwd_main(const BamAttnBwdParams* p, void* stream);
+int bam_attn_bwd_finalize(const BamAttnBwdParams* p, void* stream);
 
 /* fp32 -> bf16 conversion (dk/dv partials to the bf16 gradient layout). */
 int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "bam_mask_validate": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
     "bam_block_summarize": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "bam_classify": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "bam_count_allowed": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bam_build_tile_lists": (c_i32, [c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                      c_vp, c_vp]),
     "bam_lpt_workspace_bytes": (c_i64, [c_i64]),
@@ -60,6 +61,9 @@ SIGNATURES = {
     "bam_ilp_optimal": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "bam_attn_fwd": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp]),
     "bam_attn_bwd": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
+    "bam_attn_bwd_preprocess": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
+    "bam_attn_bwd_main": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
+    "bam_attn_bwd_finalize": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "bam_selftest_umma": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
@@ -114,6 +118,19 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+# GPU kernels each entry point launches (for the bench's gpu_launches count)
+KERNELS_PER_CALL = {
+    "bam_mask_expand": 1, "bam_mask_validate": 1, "bam_block_summarize": 1, "bam_classify": 1,
+    "bam_count_allowed": 1, "bam_build_tile_lists": 5, "bam_zigzag_assign": 1,
+    "bam_contiguous_assign": 1, "bam_split_count": 2, "bam_split_fill": 1,
+    "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
+    "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
+}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
     """Call a libbam entry point that ends with a stream argument."""
+    global launch_count
     check(getattr(load(), name)(*args, stream()))
+    launch_count += KERNELS_PER_CALL.get(name, 1)

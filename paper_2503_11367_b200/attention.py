@@ -125,12 +125,12 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None):
         plan.desc.data_ptr(), plan.q_gid.data_ptr(), plan.k_row.data_ptr(),
         plan.row_off.data_ptr(), plan.row_tiles.data_ptr(), plan.fwd_order.data_ptr(),
         plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale)
-    _lib.check(_lib.load().bam_attn_fwd(p, _lib.stream()))
+    _lib.call("bam_attn_fwd", p)
     return o, lse
 
 
 def attn_backward(q, k, v, o, lse, do, plan: AttentionPlan, scale: float | None = None,
-                  dkv_fp32: bool = False):
+                  dkv_fp32: bool = False, timer=None):
     """Returns (dq bf16, dk, dv) with dk/dv fp32 [k_rows*128, Hkv, 128]
     partials when ``dkv_fp32`` (for a CP reduce-scatter), else bf16."""
     _check_qkv(q, k, v, plan)
@@ -151,7 +151,14 @@ def attn_backward(q, k, v, o, lse, do, plan: AttentionPlan, scale: float | None 
         plan.desc.data_ptr(), plan.q_gid.data_ptr(), plan.k_row.data_ptr(),
         plan.col_off.data_ptr(), plan.col_tiles.data_ptr(), plan.bwd_order.data_ptr(),
         plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale)
-    _lib.check(_lib.load().bam_attn_bwd(p, _lib.stream()))
+    if timer is None:
+        _lib.call("bam_attn_bwd", p)
+    else:   # per-launch CUDA events around the main tcgen05 kernel (bench.py)
+        _lib.call("bam_attn_bwd_preprocess", p)
+        timer[0].record()
+        _lib.call("bam_attn_bwd_main", p)
+        timer[1].record()
+        _lib.call("bam_attn_bwd_finalize", p)
     if dkv_fp32:
         return dq, dk, dv
     return dq, to_bf16(dk), to_bf16(dv)

@@ -328,7 +328,7 @@ __global__ void bwd_dq_convert_kernel(const float4* __restrict__ acc, uint2* __r
 
 using namespace bam;
 
-extern "C" int bam_attn_bwd(const BamAttnBwdParams* pp, void* stream) {
+static int check_bwd(const BamAttnBwdParams* pp) {
   BAM_CHECK_ARG(pp != nullptr, "bam_attn_bwd: null params");
   const BamAttnBwdParams& p = *pp;
   BAM_CHECK_ARG(p.nq >= 1 && p.nb >= 1 && p.k_rows >= 1, "bam_attn_bwd: nq=%d nb=%d k_rows=%d",
@@ -336,14 +336,27 @@ extern "C" int bam_attn_bwd(const BamAttnBwdParams* pp, void* stream) {
   BAM_CHECK_ARG(p.Hq >= 1 && p.Hkv >= 1 && p.Hq % p.Hkv == 0,
                 "bam_attn_bwd: Hq=%d must be a multiple of Hkv=%d", p.Hq, p.Hkv);
   BAM_CHECK_ARG(p.nb <= 65535, "bam_attn_bwd: nb=%d > 65535", p.nb);
+  return kOk;
+}
+
+extern "C" {
+
+int bam_attn_bwd_preprocess(const BamAttnBwdParams* pp, void* stream) {
+  if (int rc = check_bwd(pp)) return rc;
+  const BamAttnBwdParams& p = *pp;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t rows = (int64_t)p.nq * 128;
-  // 1) delta = rowsum(dO * O), zero the dQ accumulator
   bwd::bwd_delta_kernel<<<148 * 8, 256, 0, s>>>((const __nv_bfloat16*)p.o,
                                                 (const __nv_bfloat16*)p.dout, rows, p.Hq, p.delta);
   BAM_LAUNCH_CHECK();
   BAM_CUDA_TRY(cudaMemsetAsync(p.dq_acc, 0, sizeof(float) * rows * p.Hq * 128, s));
-  // 2) main kernel
+  return kOk;
+}
+
+int bam_attn_bwd_main(const BamAttnBwdParams* pp, void* stream) {
+  if (int rc = check_bwd(pp)) return rc;
+  const BamAttnBwdParams& p = *pp;
+  const int64_t rows = (int64_t)p.nq * 128;
   CUtensorMap mq, mk, mv, mdo;
   int rc;
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, rows, p.Hq, 128))) return rc;
@@ -354,12 +367,26 @@ extern "C" int bam_attn_bwd(const BamAttnBwdParams* pp, void* stream) {
   BAM_CUDA_TRY(cudaFuncSetAttribute(bwd::attn_bwd_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dim3 grid(p.Hkv, p.nb);
-  bwd::attn_bwd_kernel<<<grid, bwd::kThreads, smem, s>>>(mq, mk, mv, mdo, p);
-  BAM_LAUNCH_CHECK();
-  // 3) dq = scale * dq_acc -> bf16
-  const int64_t n4 = rows * p.Hq * 32;
-  bwd::bwd_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(p.dq_acc),
-                                                     reinterpret_cast<uint2*>(p.dq), n4, p.scale);
+  bwd::attn_bwd_kernel<<<grid, bwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, mdo, p);
   BAM_LAUNCH_CHECK();
   return kOk;
 }
+
+int bam_attn_bwd_finalize(const BamAttnBwdParams* pp, void* stream) {
+  if (int rc = check_bwd(pp)) return rc;
+  const BamAttnBwdParams& p = *pp;
+  const int64_t n4 = (int64_t)p.nq * 128 * p.Hq * 32;
+  bwd::bwd_dq_convert_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(p.dq_acc), reinterpret_cast<uint2*>(p.dq), n4, p.scale);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+int bam_attn_bwd(const BamAttnBwdParams* pp, void* stream) {
+  int rc;
+  if ((rc = bam_attn_bwd_preprocess(pp, stream))) return rc;
+  if ((rc = bam_attn_bwd_main(pp, stream))) return rc;
+  return bam_attn_bwd_finalize(pp, stream);
+}
+
+}  // extern "C"

@@ -270,6 +270,38 @@ __global__ void list_fill_cols_kernel(const uint8_t* __restrict__ classes, int64
   }
 }
 
+// Exact number of allowed (q, k) pairs over all tiles (the algorithmic FLOP
+// basis): FULL tiles count |Q||K|, PARTIAL tiles are counted element-wise.
+// One CTA per query block row, one warp per tile.
+__global__ void __launch_bounds__(256) count_allowed_kernel(const int64_t* __restrict__ desc,
+                                                            const BamBlockSummary* __restrict__ sum,
+                                                            const uint8_t* __restrict__ classes,
+                                                            int64_t nb,
+                                                            unsigned long long* __restrict__ out) {
+  const int64_t row = blockIdx.x;
+  const BamBlockSummary Q = sum[row];
+  unsigned long long acc = 0;
+  for (int64_t c = threadIdx.x >> 5; c < nb; c += blockDim.x >> 5) {
+    const int cls = classes[row * nb + c];
+    if (cls == 0) continue;
+    const BamBlockSummary K = sum[c];
+    if (cls == 1) {
+      if (lane_id() == 0) acc += (unsigned long long)(Q.hi - Q.lo) * (K.hi - K.lo);
+      continue;
+    }
+    for (int64_t q = Q.lo; q < Q.hi; ++q) {
+      const long long dq = desc[q];
+      for (int64_t k0 = K.lo; k0 < K.hi; k0 += 32) {
+        const int64_t k = k0 + lane_id();
+        const bool ok = k < K.hi && bam_allowed(dq, q, desc[k < K.hi ? k : K.lo], k);
+        const uint32_t bits = __ballot_sync(0xffffffffu, ok);
+        if (lane_id() == 0) acc += __popc(bits);
+      }
+    }
+  }
+  if (lane_id() == 0 && acc) atomicAdd(out, acc);
+}
+
 static inline int grid_for(int64_t n, int threads, int cap = 148 * 16) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -317,6 +349,16 @@ int bam_classify(const int64_t* desc, const BamBlockSummary* summaries, int64_t 
                  uint8_t* classes, int32_t* W, void* stream) {
   BAM_CHECK_ARG(nb >= 1 && nb < (1ll << 31), "bam_classify: nb=%lld", (long long)nb);
   classify_kernel<<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(desc, summaries, nb, classes, W);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+int bam_count_allowed(const int64_t* desc, const BamBlockSummary* summaries,
+                      const uint8_t* classes, int64_t nb, unsigned long long* out, void* stream) {
+  BAM_CHECK_ARG(nb >= 1, "bam_count_allowed: nb=%lld", (long long)nb);
+  BAM_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(unsigned long long), (cudaStream_t)stream));
+  count_allowed_kernel<<<(unsigned)nb, 256, 0, (cudaStream_t)stream>>>(desc, summaries, classes,
+                                                                       nb, out);
   BAM_LAUNCH_CHECK();
   return kOk;
 }

@@ -250,6 +250,23 @@ def classify_device(desc: torch.Tensor, block_size: int = DEFAULT_BLOCK_SIZE):
     return classes, W
 
 
+def count_allowed(desc: torch.Tensor, block_size: int = DEFAULT_BLOCK_SIZE,
+                  classes: torch.Tensor | None = None) -> int:
+    """Exact number of (q, k) pairs with materialize() true (device count)."""
+    T = desc.shape[0]
+    nb = (T + block_size - 1) // block_size
+    summ = block_summaries(desc, block_size)
+    if classes is None:
+        classes = torch.empty(nb, nb, dtype=torch.uint8, device=desc.device)
+        W = torch.empty(nb, dtype=torch.int32, device=desc.device)
+        _lib.call("bam_classify", desc.data_ptr(), summ.data_ptr(), nb, classes.data_ptr(),
+                  W.data_ptr())
+    out = torch.empty(1, dtype=torch.int64, device=desc.device)
+    _lib.call("bam_count_allowed", desc.data_ptr(), summ.data_ptr(), classes.data_ptr(), nb,
+              out.data_ptr())
+    return int(out.item())
+
+
 def block_workloads(mask: BitfieldMask, block_size: int = DEFAULT_BLOCK_SIZE) -> BlockWorkload:
     """Classify every (query block, key block) pair and count work per row
     (mask.py:168-188).  ``skip`` pairs are fully masked, ``full`` fully
