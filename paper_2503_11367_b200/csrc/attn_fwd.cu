@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         BAM_TMEM_ST16(tmem + lane_base + kColS + c * 16, pk);
       }
-      if (rescale && t > 0) {  // O(t-1) is complete: S(t) was issued after PV(t-1) retired
+      // warp-uniform branch: tcgen05.ld/st are .sync.aligned (alpha == 1 for rows that keep m)
+      if (__any_sync(0xffffffffu, rescale) && t > 0) {  // O(t-1) complete: S(t) issued after PV(t-1)
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           uint32_t rr[32];
