@@ -4,15 +4,23 @@
 // 128-key block x one KV head and walks the CSC list of local query blocks
 // that see it (non-skip tiles only; PARTIAL tiles re-evaluate the descriptor
 // predicate of mask.py:106-112 in registers), for every query head of the
-// GQA group.  Per step (query block j, query head h):
-//   S^T  = K Q^T            (SS)  -> TMEM [0,128)     P^T = exp(S^T*scale - LSE)
-//   dP^T = V dO^T           (SS)  -> TMEM [128,256)   dS^T = P^T (dP^T - D)
-//   dQ   = dS K             (SS, both MN-major) -> TMEM [128,256) -> red.add fp32
-//   dV  += P^T dO           (TS: P^T bf16 in TMEM [0,64), dO MN-major) -> [256,384)
-//   dK  += dS^T Q           (SS: dS^T smem K-major, Q MN-major)        -> [384,512)
+// GQA group.  A step is one 64-row half of a query block for one head
+// (j outer, head, half inner, so CTAs running together hit the same dQ
+// accumulator lines in L2):
+//   S^T  = K Q^T      (SS, M=128 keys, N=64)  -> TMEM S_b      P^T = exp2(S^T c - LSE)
+//   dP^T = V dO^T     (SS)                    -> TMEM dP_b     dS^T = P^T (dP^T - D)
+//   dV  += P^T dO     (TS: P^T bf16 in S_b, dO MN-major)       -> TMEM [0,128)
+//   dK  += dS^T Q     (SS: dS^T smem K-major, Q MN-major)      -> TMEM [128,256)
+//   dQ^T = K^T dS^T   (SS: K MN-major, dS^T MN-major)          -> TMEM dP_b
+// S_b / dP_b are double-buffered (b = step & 1), so the MMAs of step s+1's
+// S/dP run while the compute warps turn step s into P / dS, and dV/dK/dQ of
+// step s run while the compute warps work on step s+1.  dQ^T puts d on the
+// TMEM lanes, so the dQ warps' fp32 reductions into dq_acc are coalesced
+// (one 128-B row segment per warp instruction).
 // Warp roles (320 threads, 1 CTA / SM):
 //   warps 0-3 compute (thread r = key row r), warps 4-7 dQ epilogue
-//   (thread r = query row r), warp 8 TMA producer, warp 9 TMEM alloc + MMA.
+//   (thread r = head-dim column r), warp 8 MMA issuer + TMEM alloc,
+//   warp 9 TMA producer (Q/dO half tiles + LSE/D into a 3-stage ring).
 #include "../../include/bam.h"
 #include "common.cuh"
 #include "tma.h"
@@ -21,30 +29,42 @@ namespace bam {
 namespace bwd {
 
 constexpr int kThreads = 320;
-constexpr uint32_t kTileBytes = 128 * 128 * 2;
-constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
+constexpr int kStages = 3;
+constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
+constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
+constexpr uint32_t kDsBytes = 128 * 64 * 2;      // dS^T: 128 key rows x 64 query cols
+constexpr uint32_t kColDV = 0, kColDK = 128, kColBuf = 256;  // buffer b: S at 256+128b, dP at +64
+
+struct Stage {
+  alignas(1024) uint8_t q[kHalfBytes];
+  alignas(1024) uint8_t dout[kHalfBytes];
+  float lse[64];
+  float delta[64];
+};
 
 struct Smem {
   alignas(1024) uint8_t k[kTileBytes];
   alignas(1024) uint8_t v[kTileBytes];
-  alignas(1024) uint8_t q[2][kTileBytes];
-  alignas(1024) uint8_t dout[2][kTileBytes];
-  alignas(1024) uint8_t ds[kTileBytes];
-  uint64_t bar_kv, bar_in_full[2], bar_in_empty[2];
-  uint64_t bar_sdp_full, bar_p_ready, bar_mma_done, bar_dq_full, bar_dq_empty;
+  alignas(1024) uint8_t ds[2][kDsBytes];
+  Stage st[kStages];
+  uint64_t bar_kv, bar_full[kStages], bar_empty[kStages];
+  uint64_t bar_sdp_full[2], bar_p_ready[2], bar_mma_done[2], bar_dq_full[2], bar_dq_empty[2];
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void load_tile(const CUtensorMap* m, uint64_t* bar, uint8_t* dst,
-                                          int head, int row0) {
-  tma_load_3d(m, bar, dst, 0, head, row0);
-  tma_load_3d(m, bar, dst + kTileBytes / 2, 64, head, row0);
+__device__ __forceinline__ void red_add(float* addr, float a) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
 }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
+struct StepInfo {
+  int h, jq, cls, half;
+};
+
+__device__ __forceinline__ StepInfo step_info(const int32_t* col, int s, int grp, int hkv) {
+  const int per_j = grp * 2;
+  const int e = col[s / per_j];
+  const int r = s % per_j;
+  return {hkv * grp + (r >> 1), e >> 2, e & 3, r & 1};
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -52,32 +72,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const BamAttnBwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                      ~uintptr_t(1023));
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int hkv = blockIdx.x;
   const int kb = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
   const int grp = p.Hq / p.Hkv;
   const int c0 = p.col_off[kb], ncol = p.col_off[kb + 1] - c0;
   const int32_t* col = p.col_tiles + c0;
-  const int nsteps = ncol * grp;
+  const int nsteps = ncol * grp * 2;
   const int64_t Tq = (int64_t)p.nq * 128;
   const int krow0 = p.k_row[kb] * 128;
 
   if (threadIdx.x == 0) {
+    if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B needs 1024-B alignment
     mbar_init(&sm.bar_kv, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.bar_in_full[i], 1);
-      mbar_init(&sm.bar_in_empty[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.bar_full[i], 1);
+      mbar_init(&sm.bar_empty[i], 1);
     }
-    mbar_init(&sm.bar_sdp_full, 1);
-    mbar_init(&sm.bar_p_ready, 128);
-    mbar_init(&sm.bar_mma_done, 1);
-    mbar_init(&sm.bar_dq_full, 1);
-    mbar_init(&sm.bar_dq_empty, 128);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.bar_sdp_full[b], 1);
+      mbar_init(&sm.bar_p_ready[b], 128);
+      mbar_init(&sm.bar_mma_done[b], 1);
+      mbar_init(&sm.bar_dq_full[b], 1);
+      mbar_init(&sm.bar_dq_empty[b], 128);
+    }
     fence_mbar_init();
   }
-  if (warp == 9) {
+  if (warp == 8) {
     tmem_alloc(&sm.tmem_base, 512);
     tmem_relinquish();
   }
@@ -86,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 8) {
+  if (warp == 9) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && nsteps > 0) {
       prefetch_tmap(&tm_q);
@@ -94,69 +116,83 @@ __global__ void __launch_bounds__(kThreads, 1)
       prefetch_tmap(&tm_v);
       prefetch_tmap(&tm_do);
       mbar_expect_tx(&sm.bar_kv, 2 * kTileBytes);
-      load_tile(&tm_k, &sm.bar_kv, sm.k, hkv, krow0);
-      load_tile(&tm_v, &sm.bar_kv, sm.v, hkv, krow0);
+      tma_load_3d(&tm_k, &sm.bar_kv, sm.k, 0, hkv, krow0);
+      tma_load_3d(&tm_k, &sm.bar_kv, sm.k + kTileBytes / 2, 64, hkv, krow0);
+      tma_load_3d(&tm_v, &sm.bar_kv, sm.v, 0, hkv, krow0);
+      tma_load_3d(&tm_v, &sm.bar_kv, sm.v + kTileBytes / 2, 64, hkv, krow0);
       for (int s = 0; s < nsteps; ++s) {
-        const int st = s & 1;
-        const int h = hkv * grp + s / ncol;
-        const int jq = col[s % ncol] >> 2;
-        if (s >= 2) mbar_wait(&sm.bar_in_empty[st], ((s >> 1) - 1) & 1);
-        mbar_expect_tx(&sm.bar_in_full[st], 2 * kTileBytes);
-        load_tile(&tm_q, &sm.bar_in_full[st], sm.q[st], h, jq * 128);
-        load_tile(&tm_do, &sm.bar_in_full[st], sm.dout[st], h, jq * 128);
+        const int st = s % kStages;
+        const StepInfo si = step_info(col, s, grp, hkv);
+        const int row0 = si.jq * 128 + si.half * 64;
+        if (s >= kStages) mbar_wait(&sm.bar_empty[st], ((s / kStages) - 1) & 1);
+        Stage& S = sm.st[st];
+        mbar_expect_tx(&sm.bar_full[st], 2 * kHalfBytes + 2 * 256);
+        tma_load_3d(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0);
+        tma_load_3d(&tm_q, &sm.bar_full[st], S.q + kHalfBytes / 2, 64, si.h, row0);
+        tma_load_3d(&tm_do, &sm.bar_full[st], S.dout, 0, si.h, row0);
+        tma_load_3d(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0);
+        bulk_load(S.lse, p.lse + (int64_t)si.h * Tq + row0, 256, &sm.bar_full[st]);
+        bulk_load(S.delta, p.delta + (int64_t)si.h * Tq + row0, 256, &sm.bar_full[st]);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && nsteps > 0) {
-      const uint32_t id_kk = idesc_bf16(128, 128, 0, 0);   // K-major A, K-major B
-      const uint32_t id_kmn = idesc_bf16(128, 128, 0, 1);  // K-major A (or TMEM), MN-major B
-      const uint32_t id_mnmn = idesc_bf16(128, 128, 1, 1); // MN-major A and B
-      const uint32_t sk = smem_u32(sm.k), sv = smem_u32(sm.v), sds = smem_u32(sm.ds);
+      const uint32_t id_s = idesc_bf16(128, 64, 0, 0);    // S^T, dP^T: K-major x K-major
+      const uint32_t id_kv = idesc_bf16(128, 128, 0, 1);  // dV, dK: (TMEM|K-major) x MN-major
+      const uint32_t id_q = idesc_bf16(128, 64, 1, 1);    // dQ^T: MN-major x MN-major
+      const uint32_t sk = smem_u32(sm.k), sv = smem_u32(sm.v);
+      auto issue_sdp = [&](int s) {
+        const int st = s % kStages, b = s & 1;
+        const uint32_t sq = smem_u32(sm.st[st].q), sdo = smem_u32(sm.st[st].dout);
+        mbar_wait(&sm.bar_full[st], (s / kStages) & 1);
+        if (s >= 2) mbar_wait(&sm.bar_mma_done[b], ((s >> 1) - 1) & 1);  // S_b (P^T), dS_b free
+        tc_fence_after();
+        const uint32_t dS = tmem + kColBuf + 128 * b, dP = dS + 64;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ka = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
+          const uint32_t kq = (kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32;
+          mma_ss(dS, sdesc_sw128(sk + ka, 16, 1024), sdesc_sw128(sq + kq, 16, 1024), id_s, kk > 0);
+        }
+        if (s >= 2) mbar_wait(&sm.bar_dq_empty[b], ((s >> 1) - 1) & 1);  // dQ^T(s-2) drained
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ka = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
+          const uint32_t kq = (kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32;
+          mma_ss(dP, sdesc_sw128(sv + ka, 16, 1024), sdesc_sw128(sdo + kq, 16, 1024), id_s, kk > 0);
+        }
+        tc_commit(&sm.bar_sdp_full[b]);
+      };
       mbar_wait(&sm.bar_kv, 0);
+      issue_sdp(0);
       for (int s = 0; s < nsteps; ++s) {
-        const int st = s & 1;
-        const uint32_t sq = smem_u32(sm.q[st]), sdo = smem_u32(sm.dout[st]);
-        mbar_wait(&sm.bar_in_full[st], (s >> 1) & 1);
-        if (s > 0) mbar_wait(&sm.bar_mma_done, (s - 1) & 1);
+        const int st = s % kStages, b = s & 1;
+        if (s + 1 < nsteps) issue_sdp(s + 1);
+        const uint32_t sq = smem_u32(sm.st[st].q), sdo = smem_u32(sm.st[st].dout);
+        const uint32_t sds = smem_u32(sm.ds[b]);
+        const uint32_t tS = tmem + kColBuf + 128 * b, tDQ = tS + 64;
+        mbar_wait(&sm.bar_p_ready[b], (s >> 1) & 1);
         tc_fence_after();
+        // dV += P^T dO   (K = 64 queries: 4 steps of 16)
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-          mma_ss(tmem + kColS, sdesc_sw128(sk + off, 16, 1024), sdesc_sw128(sq + off, 16, 1024),
-                 id_kk, kk > 0);
-        }
-        if (s > 0) mbar_wait(&sm.bar_dq_empty, (s - 1) & 1);
-        tc_fence_after();
+        for (int kk = 0; kk < 4; ++kk)
+          mma_ts(tmem + kColDV, tS + kk * 8, sdesc_sw128(sdo + kk * 2048, kHalfBytes / 2, 1024),
+                 id_kv, (s > 0 || kk > 0));
+        // dK += dS^T Q
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-          mma_ss(tmem + kColDP, sdesc_sw128(sv + off, 16, 1024), sdesc_sw128(sdo + off, 16, 1024),
-                 id_kk, kk > 0);
-        }
-        tc_commit(&sm.bar_sdp_full);
-        mbar_wait(&sm.bar_p_ready, s & 1);
-        tc_fence_after();
-        // dQ = dS K  (A = dS^T smem viewed MN-major, B = K MN-major)
+        for (int kk = 0; kk < 4; ++kk)
+          mma_ss(tmem + kColDK, sdesc_sw128(sds + kk * 32, 16, 1024),
+                 sdesc_sw128(sq + kk * 2048, kHalfBytes / 2, 1024), id_kv, (s > 0 || kk > 0));
+        // dQ^T = K^T dS^T  (K = 128 keys: 8 steps of 16 key rows)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ss(tmem + kColDP, sdesc_sw128(sds + kk * 2048, kTileBytes / 2, 1024),
-                 sdesc_sw128(sk + kk * 2048, kTileBytes / 2, 1024), id_mnmn, kk > 0);
-        tc_commit(&sm.bar_dq_full);
-        // dV += P^T dO  (A = P^T in TMEM, B = dO MN-major)
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + kColDV, tmem + kColS + kk * 8,
-                 sdesc_sw128(sdo + kk * 2048, kTileBytes / 2, 1024), id_kmn, (s > 0 || kk > 0));
-        // dK += dS^T Q  (A = dS^T smem K-major, B = Q MN-major)
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-          mma_ss(tmem + kColDK, sdesc_sw128(sds + off, 16, 1024),
-                 sdesc_sw128(sq + kk * 2048, kTileBytes / 2, 1024), id_kmn, (s > 0 || kk > 0));
-        }
-        tc_commit(&sm.bar_in_empty[st]);
-        tc_commit(&sm.bar_mma_done);
+          mma_ss(tDQ, sdesc_sw128(sk + kk * 2048, kTileBytes / 2, 1024),
+                 sdesc_sw128(sds + kk * 2048, 16, 1024), id_q, kk > 0);
+        tc_commit(&sm.bar_dq_full[b]);
+        tc_commit(&sm.bar_empty[st]);
+        tc_commit(&sm.bar_mma_done[b]);
       }
     }
   } else if (warp < 4) {
@@ -167,27 +203,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long dk = p.desc[kg];
     const float scale_log2 = p.scale * 1.4426950408889634f;
     const float log2e = 1.4426950408889634f;
-    const uint32_t ds_row = smem_u32(sm.ds) + r * 128;
     for (int s = 0; s < nsteps; ++s) {
-      const int h = hkv * grp + s / ncol;
-      const int e = col[s % ncol];
-      const int jq = e >> 2, cls = e & 3;
-      const long long qg0 = (long long)p.q_gid[jq] * 128;
-      const float* lse = p.lse + (int64_t)h * Tq + (int64_t)jq * 128;
-      const float* dlt = p.delta + (int64_t)h * Tq + (int64_t)jq * 128;
-      mbar_wait(&sm.bar_sdp_full, s & 1);
+      const int st = s % kStages, b = s & 1;
+      const StepInfo si = step_info(col, s, grp, hkv);
+      const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64;
+      const Stage& S = sm.st[st];
+      const uint32_t tS = tmem + kColBuf + 128 * b, tdP = tS + 64;
+      const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
+      mbar_wait(&sm.bar_sdp_full[b], (s >> 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t sr[32], dr[32];
-        BAM_TMEM_LD32(tmem + lane_base + kColS + c * 32, sr);
-        BAM_TMEM_LD32(tmem + lane_base + kColDP + c * 32, dr);
+        BAM_TMEM_LD32(tS + lane_base + c * 32, sr);
+        BAM_TMEM_LD32(tdP + lane_base + c * 32, dr);
         tmem_wait_ld();
         uint32_t pk[16], dsk[16];
 #pragma unroll
         for (int i4 = 0; i4 < 8; ++i4) {
-          const float4 l4 = __ldg(reinterpret_cast<const float4*>(lse + c * 32) + i4);
-          const float4 d4 = __ldg(reinterpret_cast<const float4*>(dlt + c * 32) + i4);
+          const float4 l4 = reinterpret_cast<const float4*>(S.lse + c * 32)[i4];
+          const float4 d4 = reinterpret_cast<const float4*>(S.delta + c * 32)[i4];
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
           const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
           float pv[4], dsv[4];
@@ -195,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int u = 0; u < 4; ++u) {
             const int i = i4 * 4 + u;
             float pp = ex2(fmaf(__uint_as_float(sr[i]), scale_log2, -lv[u] * log2e));
-            if (cls == 2) {
+            if (si.cls == 2) {
               const long long qg = qg0 + c * 32 + i;
               if (!bam_allowed(__ldg(p.desc + qg), qg, dk, kg)) pp = 0.f;
             }
@@ -207,36 +242,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           dsk[i4 * 2] = pack_bf16(dsv[0], dsv[1]);
           dsk[i4 * 2 + 1] = pack_bf16(dsv[2], dsv[3]);
         }
-        BAM_TMEM_ST16(tmem + lane_base + kColS + c * 16, pk);
-        // dS^T row r, columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
+        BAM_TMEM_ST16(tS + lane_base + c * 16, pk);
+        // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t colq = c * 32 + q4 * 8;
-          const uint32_t box = colq >> 6;
-          const uint32_t chunk = ((colq & 63) >> 3) ^ (r & 7);
-          const uint32_t addr = ds_row + box * (kTileBytes / 2) + chunk * 16;
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(dsk[q4 * 4]),
-                       "r"(dsk[q4 * 4 + 1]), "r"(dsk[q4 * 4 + 2]), "r"(dsk[q4 * 4 + 3])
+          const uint32_t chunk = (uint32_t)(c * 4 + q4) ^ (uint32_t)(r & 7);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ds_row + chunk * 16),
+                       "r"(dsk[q4 * 4]), "r"(dsk[q4 * 4 + 1]), "r"(dsk[q4 * 4 + 2]),
+                       "r"(dsk[q4 * 4 + 3])
                        : "memory");
         }
       }
       tmem_wait_st();
       fence_async_smem();
       tc_fence_before();
-      mbar_arrive(&sm.bar_p_ready);
+      mbar_arrive(&sm.bar_p_ready[b]);
     }
     // epilogue: dV, dK (scaled) -> fp32 rows of the key block
     const int64_t row = (int64_t)krow0 + r;
     float* dvrow = p.dv + (row * p.Hkv + hkv) * 128;
     float* dkrow = p.dk + (row * p.Hkv + hkv) * 128;
     if (nsteps > 0) {
-      mbar_wait(&sm.bar_mma_done, (nsteps - 1) & 1);
+      mbar_wait(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t a[32], b[32];
+        uint32_t a[32], bb[32];
         BAM_TMEM_LD32(tmem + lane_base + kColDV + c * 32, a);
-        BAM_TMEM_LD32(tmem + lane_base + kColDK + c * 32, b);
+        BAM_TMEM_LD32(tmem + lane_base + kColDK + c * 32, bb);
         tmem_wait_ld();
         float4* dv4 = reinterpret_cast<float4*>(dvrow + c * 32);
         float4* dk4 = reinterpret_cast<float4*>(dkrow + c * 32);
@@ -244,8 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 8; ++i) {
           dv4[i] = make_float4(__uint_as_float(a[4 * i]), __uint_as_float(a[4 * i + 1]),
                                __uint_as_float(a[4 * i + 2]), __uint_as_float(a[4 * i + 3]));
-          dk4[i] = make_float4(__uint_as_float(b[4 * i]) * p.scale, __uint_as_float(b[4 * i + 1]) * p.scale,
-                               __uint_as_float(b[4 * i + 2]) * p.scale, __uint_as_float(b[4 * i + 3]) * p.scale);
+          dk4[i] = make_float4(__uint_as_float(bb[4 * i]) * p.scale,
+                               __uint_as_float(bb[4 * i + 1]) * p.scale,
+                               __uint_as_float(bb[4 * i + 2]) * p.scale,
+                               __uint_as_float(bb[4 * i + 3]) * p.scale);
         }
       }
     } else {
@@ -258,31 +293,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ dQ epilogue warps 4-7
-    const int r = (warp - 4) * 32 + lane;
+    // TMEM lane = head-dim column d; columns = the 64 queries of the step.
+    const int d = (warp - 4) * 32 + lane;
     const uint32_t lane_base = ((warp - 4) * 32) << 16;
     for (int s = 0; s < nsteps; ++s) {
-      const int h = hkv * grp + s / ncol;
-      const int jq = col[s % ncol] >> 2;
-      float* dst = p.dq_acc + (((int64_t)jq * 128 + r) * p.Hq + h) * 128;
-      mbar_wait(&sm.bar_dq_full, s & 1);
+      const int b = s & 1;
+      const StepInfo si = step_info(col, s, grp, hkv);
+      float* dst = p.dq_acc + ((int64_t)(si.jq * 128 + si.half * 64) * p.Hq + si.h) * 128 + d;
+      const int64_t qstride = (int64_t)p.Hq * 128;
+      const uint32_t tDQ = tmem + kColBuf + 128 * b + 64;
+      mbar_wait(&sm.bar_dq_full[b], (s >> 1) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t a[32];
-        BAM_TMEM_LD32(tmem + lane_base + kColDP + c * 32, a);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          red_add_v4(dst + c * 32 + 4 * i, __uint_as_float(a[4 * i]), __uint_as_float(a[4 * i + 1]),
-                     __uint_as_float(a[4 * i + 2]), __uint_as_float(a[4 * i + 3]));
-      }
+      uint32_t a[32], c2[32];
+      BAM_TMEM_LD32(tDQ + lane_base, a);
+      BAM_TMEM_LD32(tDQ + lane_base + 32, c2);
+      tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&sm.bar_dq_empty);
+      mbar_arrive(&sm.bar_dq_empty[b]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        red_add(dst, __uint_as_float(a[i]));
+        dst += qstride;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        red_add(dst, __uint_as_float(c2[i]));
+        dst += qstride;
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -359,11 +401,11 @@ int bam_attn_bwd_main(const BamAttnBwdParams* pp, void* stream) {
   const int64_t rows = (int64_t)p.nq * 128;
   CUtensorMap mq, mk, mv, mdo;
   int rc;
-  if ((rc = make_tmap_rows_heads_d128(&mq, p.q, rows, p.Hq, 128))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mdo, p.dout, rows, p.Hq, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mq, p.q, rows, p.Hq, 64))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mdo, p.dout, rows, p.Hq, 64))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
-  const int smem = (int)sizeof(bwd::Smem) + 1024;
+  const int smem = (int)sizeof(bwd::Smem);
   BAM_CUDA_TRY(cudaFuncSetAttribute(bwd::attn_bwd_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dim3 grid(p.Hkv, p.nb);
