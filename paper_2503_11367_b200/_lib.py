@@ -14,7 +14,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbam.so")
+LIB_PATH = os.environ.get("BAM_LIB_PATH") or os.path.join(_PKG, "libbam.so")
 
 c_i32, c_i64, c_f32, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
 

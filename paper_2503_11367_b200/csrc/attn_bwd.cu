@@ -38,8 +38,7 @@ constexpr uint32_t kColDV = 0, kColDK = 128, kColBuf = 256;  // buffer b: S at 2
 struct Stage {
   alignas(1024) uint8_t q[kHalfBytes];
   alignas(1024) uint8_t dout[kHalfBytes];
-  float lse[64];
-  float delta[64];
+  float ld[128];   // (lse * log2e, delta) pairs for the 64 queries
 };
 
 struct Smem {
@@ -126,13 +125,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row0 = si.jq * 128 + si.half * 64;
         if (s >= kStages) mbar_wait(&sm.bar_empty[st], ((s / kStages) - 1) & 1);
         Stage& S = sm.st[st];
-        mbar_expect_tx(&sm.bar_full[st], 2 * kHalfBytes + 2 * 256);
+        mbar_expect_tx(&sm.bar_full[st], 2 * kHalfBytes + 512);
         tma_load_3d(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0);
         tma_load_3d(&tm_q, &sm.bar_full[st], S.q + kHalfBytes / 2, 64, si.h, row0);
         tma_load_3d(&tm_do, &sm.bar_full[st], S.dout, 0, si.h, row0);
         tma_load_3d(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0);
-        bulk_load(S.lse, p.lse + (int64_t)si.h * Tq + row0, 256, &sm.bar_full[st]);
-        bulk_load(S.delta, p.delta + (int64_t)si.h * Tq + row0, 256, &sm.bar_full[st]);
+        bulk_load(S.ld, p.delta + 2 * ((int64_t)si.h * Tq + row0), 512, &sm.bar_full[st]);
       }
     }
   } else if (warp == 8) {
@@ -146,7 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int st = s % kStages, b = s & 1;
         const uint32_t sq = smem_u32(sm.st[st].q), sdo = smem_u32(sm.st[st].dout);
         mbar_wait(&sm.bar_full[st], (s / kStages) & 1);
-        if (s >= 2) mbar_wait(&sm.bar_mma_done[b], ((s >> 1) - 1) & 1);  // S_b (P^T), dS_b free
+        // S_b still holds P^T(s-2), read by dV(s-2): issued earlier by this thread, and
+        // tcgen05.mma ops from one thread execute in issue order, so no wait is needed.
         tc_fence_after();
         const uint32_t dS = tmem + kColBuf + 128 * b, dP = dS + 64;
 #pragma unroll
@@ -202,47 +201,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long kg = (long long)kb * 128 + r;
     const long long dk = p.desc[kg];
     const float scale_log2 = p.scale * 1.4426950408889634f;
-    const float log2e = 1.4426950408889634f;
     for (int s = 0; s < nsteps; ++s) {
       const int st = s % kStages, b = s & 1;
       const StepInfo si = step_info(col, s, grp, hkv);
-      const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64;
       const Stage& S = sm.st[st];
-      const uint32_t tS = tmem + kColBuf + 128 * b, tdP = tS + 64;
+      const uint32_t tS = tmem + kColBuf + 128 * b + lane_base, tdP = tS + 64;
       const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
       mbar_wait(&sm.bar_sdp_full[b], (s >> 1) & 1);
       tc_fence_after();
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t sr[32], dr[32];
-        BAM_TMEM_LD32(tS + lane_base + c * 32, sr);
-        BAM_TMEM_LD32(tdP + lane_base + c * 32, dr);
+        BAM_TMEM_LD32(tS + c * 32, sr);
+        BAM_TMEM_LD32(tdP + c * 32, dr);
+        uint32_t allow = 0xFFFFFFFFu;
+        if (si.cls == 2) {  // PARTIAL tile: descriptor predicate for these 32 queries
+          const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64 + c * 32;
+          allow = 0;
+#pragma unroll 1
+          for (int i = 0; i < 32; ++i)
+            allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
+        }
         tmem_wait_ld();
+        const float4* ld = reinterpret_cast<const float4*>(S.ld + c * 64);  // (lse*log2e, D) pairs
         uint32_t pk[16], dsk[16];
 #pragma unroll
-        for (int i4 = 0; i4 < 8; ++i4) {
-          const float4 l4 = reinterpret_cast<const float4*>(S.lse + c * 32)[i4];
-          const float4 d4 = reinterpret_cast<const float4*>(S.delta + c * 32)[i4];
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-          float pv[4], dsv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = i4 * 4 + u;
-            float pp = ex2(fmaf(__uint_as_float(sr[i]), scale_log2, -lv[u] * log2e));
-            if (si.cls == 2) {
-              const long long qg = qg0 + c * 32 + i;
-              if (!bam_allowed(__ldg(p.desc + qg), qg, dk, kg)) pp = 0.f;
-            }
-            pv[u] = pp;
-            dsv[u] = pp * (__uint_as_float(dr[i]) - dv[u]);
-          }
-          pk[i4 * 2] = pack_bf16(pv[0], pv[1]);
-          pk[i4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
-          dsk[i4 * 2] = pack_bf16(dsv[0], dsv[1]);
-          dsk[i4 * 2 + 1] = pack_bf16(dsv[2], dsv[3]);
+        for (int i2 = 0; i2 < 16; ++i2) {
+          const float4 v = ld[i2];
+          float p0 = ex2(fmaf(__uint_as_float(sr[2 * i2]), scale_log2, -v.x));
+          float p1 = ex2(fmaf(__uint_as_float(sr[2 * i2 + 1]), scale_log2, -v.z));
+          p0 = (allow >> (2 * i2)) & 1 ? p0 : 0.f;
+          p1 = (allow >> (2 * i2 + 1)) & 1 ? p1 : 0.f;
+          pk[i2] = pack_bf16(p0, p1);
+          dsk[i2] = pack_bf16(p0 * (__uint_as_float(dr[2 * i2]) - v.y),
+                              p1 * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
         }
-        BAM_TMEM_ST16(tS + lane_base + c * 16, pk);
+        BAM_TMEM_ST16(tS + c * 16, pk);
         // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
@@ -265,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (nsteps > 0) {
       mbar_wait(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
       tc_fence_after();
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t a[32], bb[32];
         BAM_TMEM_LD32(tmem + lane_base + kColDV + c * 32, a);
@@ -310,6 +304,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&sm.bar_dq_empty[b]);
+#ifdef BAM_EXPERIMENT_NO_DQ_RED
+      if (a[0] == 0x7fc00001u) red_add(dst, 1.f);   // keep the loads live, skip the reductions
+      continue;
+#endif
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         red_add(dst, __uint_as_float(a[i]));
@@ -330,10 +328,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// delta[h, row] = sum_d dO[row, h, d] * O[row, h, d]   (one warp per (row, h))
+// ld[h, row] = (lse[h, row] * log2e, sum_d dO[row, h, d] * O[row, h, d])  (one warp per (row, h))
 __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
-                                 const __nv_bfloat16* __restrict__ dout, int64_t rows, int H,
-                                 float* __restrict__ delta) {
+                                 const __nv_bfloat16* __restrict__ dout,
+                                 const float* __restrict__ lse, int64_t rows, int H,
+                                 float2* __restrict__ ld) {
   const int64_t nw = rows * H;
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -350,7 +349,7 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
     for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
     if (lane_id() == 0) {
       const int64_t row = w / H, h = w % H;
-      delta[h * rows + row] = acc;
+      ld[h * rows + row] = make_float2(lse[h * rows + row] * 1.4426950408889634f, acc);
     }
   }
 }
@@ -389,7 +388,8 @@ int bam_attn_bwd_preprocess(const BamAttnBwdParams* pp, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t rows = (int64_t)p.nq * 128;
   bwd::bwd_delta_kernel<<<148 * 8, 256, 0, s>>>((const __nv_bfloat16*)p.o,
-                                                (const __nv_bfloat16*)p.dout, rows, p.Hq, p.delta);
+                                                (const __nv_bfloat16*)p.dout, p.lse, rows, p.Hq,
+                                                reinterpret_cast<float2*>(p.delta));
   BAM_LAUNCH_CHECK();
   BAM_CUDA_TRY(cudaMemsetAsync(p.dq_acc, 0, sizeof(float) * rows * p.Hq * 128, s));
   return kOk;
