@@ -17,10 +17,11 @@
 // step s run while the compute warps work on step s+1.  dQ^T puts d on the
 // TMEM lanes, so the dQ warps' fp32 reductions into dq_acc are coalesced
 // (one 128-B row segment per warp instruction).
+// Q/dO half tiles stream through a 4-stage TMA ring.
 // Warp roles (320 threads, 1 CTA / SM):
 //   warps 0-3 compute (thread r = key row r), warps 4-7 dQ epilogue
 //   (thread r = head-dim column r), warp 8 MMA issuer + TMEM alloc,
-//   warp 9 TMA producer (Q/dO half tiles + LSE/D into a 3-stage ring).
+//   warp 9 TMA producer (Q/dO half tiles + LSE/D pairs).
 #include "../../include/bam.h"
 #include "common.cuh"
 #include "tma.h"
@@ -29,7 +30,7 @@ namespace bam {
 namespace bwd {
 
 constexpr int kThreads = 320;
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
 constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
 constexpr uint32_t kDsBytes = 128 * 64 * 2;      // dS^T: 128 key rows x 64 query cols
@@ -38,7 +39,6 @@ constexpr uint32_t kColDV = 0, kColDK = 128, kColBuf = 256;  // buffer b: S at 2
 struct Stage {
   alignas(1024) uint8_t q[kHalfBytes];
   alignas(1024) uint8_t dout[kHalfBytes];
-  float ld[128];   // (lse * log2e, delta) pairs for the 64 queries
 };
 
 struct Smem {
@@ -46,6 +46,7 @@ struct Smem {
   alignas(1024) uint8_t v[kTileBytes];
   alignas(1024) uint8_t ds[2][kDsBytes];
   Stage st[kStages];
+  alignas(16) float ld[kStages][128];   // per stage: (lse * log2e, delta) pairs, 64 queries
   uint64_t bar_kv, bar_full[kStages], bar_empty[kStages];
   uint64_t bar_sdp_full[2], bar_p_ready[2], bar_mma_done[2], bar_dq_full[2], bar_dq_empty[2];
   uint32_t tmem_base;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(&tm_q, &sm.bar_full[st], S.q + kHalfBytes / 2, 64, si.h, row0);
         tma_load_3d(&tm_do, &sm.bar_full[st], S.dout, 0, si.h, row0);
         tma_load_3d(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0);
-        bulk_load(S.ld, p.delta + 2 * ((int64_t)si.h * Tq + row0), 512, &sm.bar_full[st]);
+        bulk_load(sm.ld[st], p.delta + 2 * ((int64_t)si.h * Tq + row0), 512, &sm.bar_full[st]);
       }
     }
   } else if (warp == 8) {
@@ -204,7 +205,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < nsteps; ++s) {
       const int st = s % kStages, b = s & 1;
       const StepInfo si = step_info(col, s, grp, hkv);
-      const Stage& S = sm.st[st];
       const uint32_t tS = tmem + kColBuf + 128 * b + lane_base, tdP = tS + 64;
       const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
       mbar_wait(&sm.bar_sdp_full[b], (s >> 1) & 1);
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
         }
         tmem_wait_ld();
-        const float4* ld = reinterpret_cast<const float4*>(S.ld + c * 64);  // (lse*log2e, D) pairs
+        const float4* ld = reinterpret_cast<const float4*>(sm.ld[st] + c * 64);  // (lse*log2e, D)
         uint32_t pk[16], dsk[16];
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
