@@ -1,0 +1,79 @@
+"""GPU parity of the context-parallel plan on one device: CP ranks are
+emulated one after another (the ranks' kernels never wait on each other, the
+only exchange is NCCL), with the all-gather replaced by placing every global
+block at its gathered row and the reduce-scatter by summing the partials.
+Exercises the non-identity q_gid / k_row mappings of the kernels for every
+distribution policy.  The real NCCL path runs under torchrun in
+tools/cp_check.py and bench.py --gpus N."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention_ref, mask_ref
+
+pytestmark = pytest.mark.gpu
+
+BLOCK = 128
+
+
+def rel_l2(a, b):
+    a, b = a.float().cpu(), b.float().cpu()
+    return ((a - b).norm() / b.norm()).item()
+
+
+@pytest.mark.parametrize("policy,world", [("lpt", 4), ("zigzag", 2), ("contiguous", 3)])
+def test_cp_emulated_ranks(policy, world):
+    from paper_2503_11367_b200 import attention as A
+    from paper_2503_11367_b200 import cp
+
+    segs = [("text", 256), ("img0", 512), ("text", 384), ("img1", 256), ("text", 640)]
+    desc_l, _ = mask_ref.build_bitfield(segs)
+    desc = np.asarray(desc_l, np.int64)
+    T = desc.shape[0]
+    Hq, Hkv = 4, 2
+    g = torch.Generator().manual_seed(1234)
+    q = torch.randn(T, Hq, 128, generator=g).to(torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, generator=g).to(torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, generator=g).to(torch.bfloat16)
+    do = torch.randn(T, Hq, 128, generator=g).to(torch.bfloat16)
+    dev = torch.device("cuda")
+    d_desc = torch.from_numpy(desc).to(dev)
+    qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
+    o_ref, lse_ref = attention_ref.attention_fwd(q, k, v, desc, np.arange(T))
+    dq_ref, dk_ref, dv_ref = attention_ref.attention_bwd(q, k, v, o_ref, lse_ref, do, desc,
+                                                         np.arange(T))
+    dk_sum = torch.zeros(T, Hkv, 128)
+    dv_sum = torch.zeros(T, Hkv, 128)
+    loads = []
+    for rank in range(world):
+        plan = cp.make_cp_plan(d_desc, world, rank, policy)
+        lay = plan.layout
+        loads.append(plan.assignment.loads.cpu().tolist())
+        krow = lay.k_row.to(torch.int64)
+        idx = (krow[:, None] * BLOCK + torch.arange(BLOCK, device=dev)[None, :]).reshape(-1)
+        rows = world * lay.max_blocks * BLOCK
+        k_all = torch.zeros(rows, Hkv, 128, dtype=torch.bfloat16, device=dev)
+        v_all = torch.zeros_like(k_all)
+        k_all[idx] = kd
+        v_all[idx] = vd
+        q_loc, do_loc = cp.shard_rows(qd, lay).contiguous(), cp.shard_rows(dod, lay).contiguous()
+        o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn)
+        dq, dk_all, dv_all = A.attn_backward(q_loc, k_all, v_all, o, lse, do_loc, plan.attn,
+                                             dkv_fp32=True)
+        torch.cuda.synchronize()
+        pos = (lay.local_blocks.cpu().to(torch.int64)[:, None] * BLOCK +
+               torch.arange(BLOCK)[None, :]).reshape(-1)
+        assert rel_l2(o, o_ref[pos]) < 1e-2
+        assert (o.float().cpu() - o_ref[pos]).abs().max() < 2e-2
+        assert rel_l2(dq, dq_ref[pos]) < 1e-2
+        dk_sum += dk_all[idx].cpu()
+        dv_sum += dv_all[idx].cpu()
+    assert rel_l2(dk_sum, dk_ref) < 1e-2 and (dk_sum - dk_ref).abs().max() < 2e-2
+    assert rel_l2(dv_sum, dv_ref) < 1e-2 and (dv_sum - dv_ref).abs().max() < 2e-2
+    # the device assignment is the reference policy, bit-exact
+    from oracle import balance_ref
+    _, W = mask_ref.block_workloads_np(desc, BLOCK)
+    ref = {"lpt": balance_ref.lpt, "zigzag": balance_ref.zigzag,
+           "contiguous": balance_ref.contiguous}[policy](list(W), world)
+    assert tuple(loads[0]) == ref[1]
