@@ -109,90 +109,102 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 9) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && nsteps > 0) {
-      prefetch_tmap(&tm_q);
-      prefetch_tmap(&tm_k);
-      prefetch_tmap(&tm_v);
-      prefetch_tmap(&tm_do);
-      mbar_expect_tx(&sm.bar_kv, 2 * kTileBytes);
-      tma_load_3d(&tm_k, &sm.bar_kv, sm.k, 0, hkv, krow0);
-      tma_load_3d(&tm_k, &sm.bar_kv, sm.k + kTileBytes / 2, 64, hkv, krow0);
-      tma_load_3d(&tm_v, &sm.bar_kv, sm.v, 0, hkv, krow0);
-      tma_load_3d(&tm_v, &sm.bar_kv, sm.v + kTileBytes / 2, 64, hkv, krow0);
+    // ------------------------------------------------------------ TMA producer (whole warp)
+    const uint32_t leader = elect_one();
+    if (nsteps > 0) {
+      if (leader) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+        prefetch_tmap(&tm_do);
+      }
+      mbar_expect_tx_w(&sm.bar_kv, 2 * kTileBytes, leader);
+      tma_load_3d_w(&tm_k, &sm.bar_kv, sm.k, 0, hkv, krow0, leader);
+      tma_load_3d_w(&tm_k, &sm.bar_kv, sm.k + kTileBytes / 2, 64, hkv, krow0, leader);
+      tma_load_3d_w(&tm_v, &sm.bar_kv, sm.v, 0, hkv, krow0, leader);
+      tma_load_3d_w(&tm_v, &sm.bar_kv, sm.v + kTileBytes / 2, 64, hkv, krow0, leader);
       for (int s = 0; s < nsteps; ++s) {
         const int st = s % kStages;
         const StepInfo si = step_info(col, s, grp, hkv);
         const int row0 = si.jq * 128 + si.half * 64;
         if (s >= kStages) mbar_wait(&sm.bar_empty[st], ((s / kStages) - 1) & 1);
         Stage& S = sm.st[st];
-        mbar_expect_tx(&sm.bar_full[st], 2 * kHalfBytes + 512);
-        tma_load_3d(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0);
-        tma_load_3d(&tm_q, &sm.bar_full[st], S.q + kHalfBytes / 2, 64, si.h, row0);
-        tma_load_3d(&tm_do, &sm.bar_full[st], S.dout, 0, si.h, row0);
-        tma_load_3d(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0);
-        bulk_load(sm.ld[st], p.delta + 2 * ((int64_t)si.h * Tq + row0), 512, &sm.bar_full[st]);
+        mbar_expect_tx_w(&sm.bar_full[st], 2 * kHalfBytes + 512, leader);
+        tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0, leader);
+        tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q + kHalfBytes / 2, 64, si.h, row0, leader);
+        tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout, 0, si.h, row0, leader);
+        tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0, leader);
+        bulk_load_w(sm.ld[st], p.delta + 2 * ((int64_t)si.h * Tq + row0), 512, &sm.bar_full[st],
+                    leader);
       }
     }
   } else if (warp == 8) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && nsteps > 0) {
+    // ------------------------------------------------------------ MMA issuer (whole warp)
+    // Descriptors are built once; per MMA only the 14-bit start-address field
+    // advances (adding offset >> 4 to the 64-bit descriptor cannot carry out).
+    const uint32_t leader = elect_one();
+    if (nsteps > 0) {
       const uint32_t id_s = idesc_bf16(128, 64, 0, 0);    // S^T, dP^T: K-major x K-major
       const uint32_t id_kv = idesc_bf16(128, 128, 0, 1);  // dV, dK: (TMEM|K-major) x MN-major
       const uint32_t id_q = idesc_bf16(128, 64, 1, 1);    // dQ^T: MN-major x MN-major
-      const uint32_t sk = smem_u32(sm.k), sv = smem_u32(sm.v);
+      const uint64_t dk_k = sdesc_sw128(smem_u32(sm.k), 16, 1024);            // K, K-major
+      const uint64_t dk_v = sdesc_sw128(smem_u32(sm.v), 16, 1024);            // V, K-major
+      const uint64_t dk_kmn = sdesc_sw128(smem_u32(sm.k), kTileBytes / 2, 1024);  // K, MN-major
+      const uint64_t d_q0 = sdesc_sw128(smem_u32(sm.st[0].q), 16, 1024);         // K-major
+      const uint64_t d_q0mn = sdesc_sw128(smem_u32(sm.st[0].q), kHalfBytes / 2, 1024);
+      const uint64_t d_ds0 = sdesc_sw128(smem_u32(sm.ds[0]), 16, 1024);
+      constexpr uint32_t kStage16 = sizeof(Stage) >> 4, kDo16 = kHalfBytes >> 4;
+      constexpr uint32_t kDs16 = kDsBytes >> 4;
       auto issue_sdp = [&](int s) {
         const int st = s % kStages, b = s & 1;
-        const uint32_t sq = smem_u32(sm.st[st].q), sdo = smem_u32(sm.st[st].dout);
         mbar_wait(&sm.bar_full[st], (s / kStages) & 1);
-        // S_b still holds P^T(s-2), read by dV(s-2): issued earlier by this thread, and
+        // S_b still holds P^T(s-2), read by dV(s-2): issued earlier by this warp, and
         // tcgen05.mma ops from one thread execute in issue order, so no wait is needed.
         tc_fence_after();
-        const uint32_t dS = tmem + kColBuf + 128 * b, dP = dS + 64;
+        const uint32_t tS = tmem + kColBuf + 128 * b, tdP = tS + 64;
+        const uint64_t dq = d_q0 + st * kStage16, ddo = dq + kDo16;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t ka = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-          const uint32_t kq = (kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32;
-          mma_ss(dS, sdesc_sw128(sk + ka, 16, 1024), sdesc_sw128(sq + kq, 16, 1024), id_s, kk > 0);
+          const uint32_t ka = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
+          const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
+          mma_ss_w(tS, dk_k + ka, dq + kq, id_s, kk > 0, leader);
         }
         if (s >= 2) mbar_wait(&sm.bar_dq_empty[b], ((s >> 1) - 1) & 1);  // dQ^T(s-2) drained
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t ka = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-          const uint32_t kq = (kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32;
-          mma_ss(dP, sdesc_sw128(sv + ka, 16, 1024), sdesc_sw128(sdo + kq, 16, 1024), id_s, kk > 0);
+          const uint32_t ka = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
+          const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
+          mma_ss_w(tdP, dk_v + ka, ddo + kq, id_s, kk > 0, leader);
         }
-        tc_commit(&sm.bar_sdp_full[b]);
+        tc_commit_w(&sm.bar_sdp_full[b], leader);
       };
       mbar_wait(&sm.bar_kv, 0);
       issue_sdp(0);
       for (int s = 0; s < nsteps; ++s) {
         const int st = s % kStages, b = s & 1;
         if (s + 1 < nsteps) issue_sdp(s + 1);
-        const uint32_t sq = smem_u32(sm.st[st].q), sdo = smem_u32(sm.st[st].dout);
-        const uint32_t sds = smem_u32(sm.ds[b]);
+        const uint64_t dqmn = d_q0mn + st * kStage16, ddomn = dqmn + kDo16;
+        const uint64_t dds = d_ds0 + b * kDs16;
         const uint32_t tS = tmem + kColBuf + 128 * b, tDQ = tS + 64;
         mbar_wait(&sm.bar_p_ready[b], (s >> 1) & 1);
         tc_fence_after();
-        // dV += P^T dO   (K = 64 queries: 4 steps of 16)
+        // dV += P^T dO   (K = 64 queries: 4 steps of 16 rows = 2048 B)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ts(tmem + kColDV, tS + kk * 8, sdesc_sw128(sdo + kk * 2048, kHalfBytes / 2, 1024),
-                 id_kv, (s > 0 || kk > 0));
-        // dK += dS^T Q
+          mma_ts_w(tmem + kColDV, tS + kk * 8, ddomn + kk * 128, id_kv, (s > 0 || kk > 0), leader);
+        // dK += dS^T Q   (dS^T K-major: 32 B per 16 queries)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ss(tmem + kColDK, sdesc_sw128(sds + kk * 32, 16, 1024),
-                 sdesc_sw128(sq + kk * 2048, kHalfBytes / 2, 1024), id_kv, (s > 0 || kk > 0));
-        // dQ^T = K^T dS^T  (K = 128 keys: 8 steps of 16 key rows)
+          mma_ss_w(tmem + kColDK, dds + kk * 2, dqmn + kk * 128, id_kv, (s > 0 || kk > 0), leader);
+        // dQ^T = K^T dS^T  (K = 128 keys: 8 steps of 16 key rows = 2048 B); dS^T as MN-major
+        // B uses the same start address with LBO unused (N = 64 = one swizzle atom)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ss(tDQ, sdesc_sw128(sk + kk * 2048, kTileBytes / 2, 1024),
-                 sdesc_sw128(sds + kk * 2048, 16, 1024), id_q, kk > 0);
-        tc_commit(&sm.bar_dq_full[b]);
-        tc_commit(&sm.bar_empty[st]);
-        tc_commit(&sm.bar_mma_done[b]);
+          mma_ss_w(tDQ, dk_kmn + kk * 128, dds + kk * 128, id_q, kk > 0, leader);
+        tc_commit_w(&sm.bar_dq_full[b], leader);
+        tc_commit_w(&sm.bar_empty[st], leader);
+        tc_commit_w(&sm.bar_mma_done[b], leader);
       }
     }
   } else if (warp < 4) {
