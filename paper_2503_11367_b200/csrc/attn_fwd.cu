@@ -42,6 +42,124 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* m, uint64_t* bar, u
   tma_load_3d(m, bar, dst + kTileBytes / 2, 64, head, row0);
 }
 
+// Softmax / epilogue role of one 128-row query tile: thread (warp w, lane)
+// owns row r = 32 w + lane = TMEM lane r.  Per key tile t: wait S(t), mask
+// PARTIAL tiles, online softmax (log2 domain, lazy 2^8 rescale of O in TMEM),
+// P -> bf16 into the S columns, arrive p_ready.  Finally O / l -> bf16, LSE.
+__device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t tmem,
+                                             uint32_t colS, uint32_t colO, uint64_t* bar_s_full,
+                                             uint64_t* bar_p_ready, uint64_t* bar_pv_done, int j,
+                                             int h, uint32_t warp, uint32_t lane,
+                                             const int32_t* tiles, int n) {
+  const int r = (warp & 3) * 32 + lane;
+  const uint32_t lane_base = ((warp & 3) * 32) << 16;
+  const long long qg = (long long)p.q_gid[j] * 128 + r;
+  const long long dq = p.desc[qg];
+  const float scale_log2 = p.scale * 1.4426950408889634f;
+  float m = -INFINITY, l = 0.f;
+  for (int t = 0; t < n; ++t) {
+    const int e = tiles[t];
+    const int cls = e & 3;
+    const long long kg0 = (long long)(e >> 2) * 128;
+    mbar_wait(bar_s_full, t & 1);
+    tc_fence_after();
+    float s[128];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t rr[32];
+      BAM_TMEM_LD32(tmem + lane_base + colS + c * 32, rr);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(rr[i]);
+    }
+    if (cls == 2) {  // PARTIAL: descriptor predicate per element, 32 columns at a time
+      const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t bits = 0;
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+          const long long d = __ldg(dk + c * 32 + i);
+          bits |= uint32_t(bam_allowed(dq, qg, d, kg0 + c * 32 + i)) << i;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (!((bits >> i) & 1)) s[c * 32 + i] = -INFINITY;
+      }
+    }
+    float mt = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 128; ++c) mt = fmaxf(mt, s[c]);
+    const float m_new = fmaxf(m, mt * scale_log2);
+    // lazy rescale: only when the running max grows by more than 2^8
+    const bool rescale = m_new > m + 8.f;
+    const float alpha = rescale ? ex2(m - m_new) : 1.f;  // m = -inf -> 0
+    if (rescale) {
+      l *= alpha;
+      m = m_new;
+    }
+    const float mb = (m == -INFINITY) ? 0.f : m;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float p0 = ex2(fmaf(s[c * 32 + 2 * i], scale_log2, -mb));
+        const float p1 = ex2(fmaf(s[c * 32 + 2 * i + 1], scale_log2, -mb));
+        l += p0 + p1;
+        pk[i] = pack_bf16(p0, p1);
+      }
+      BAM_TMEM_ST16(tmem + lane_base + colS + c * 16, pk);
+    }
+    // warp-uniform branch: tcgen05.ld/st are .sync.aligned (alpha == 1 for rows that keep m).
+    // O(t-1) is complete: S(t) was issued after PV(t-1) and its commit covers it.
+    if (__any_sync(0xffffffffu, rescale) && t > 0) {
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rr[32];
+        BAM_TMEM_LD32(tmem + lane_base + colO + c * 32, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+        BAM_TMEM_ST32(tmem + lane_base + colO + c * 32, rr);
+      }
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    mbar_arrive(bar_p_ready);
+  }
+  // epilogue: O / l -> bf16, LSE
+  const int64_t Tq = (int64_t)p.nq * 128;
+  const int64_t row = (int64_t)j * 128 + r;
+  __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + (row * p.Hq + h) * 128;
+  if (n > 0) {
+    mbar_wait(bar_pv_done, (n - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t rr[32];
+      BAM_TMEM_LD32(tmem + lane_base + colO + c * 32, rr);
+      tmem_wait_ld();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 v;
+        v.x = pack_bf16(__uint_as_float(rr[8 * i + 0]) * inv, __uint_as_float(rr[8 * i + 1]) * inv);
+        v.y = pack_bf16(__uint_as_float(rr[8 * i + 2]) * inv, __uint_as_float(rr[8 * i + 3]) * inv);
+        v.z = pack_bf16(__uint_as_float(rr[8 * i + 4]) * inv, __uint_as_float(rr[8 * i + 5]) * inv);
+        v.w = pack_bf16(__uint_as_float(rr[8 * i + 6]) * inv, __uint_as_float(rr[8 * i + 7]) * inv);
+        dst[i] = v;
+      }
+    }
+    p.lse[(int64_t)h * Tq + row] = l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(orow);
+    for (int i = 0; i < 16; ++i) dst[i] = make_uint4(0, 0, 0, 0);
+    p.lse[(int64_t)h * Tq + row] = -INFINITY;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p) {
@@ -76,29 +194,38 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && n > 0) {
-      prefetch_tmap(&tm_q);
-      prefetch_tmap(&tm_k);
-      prefetch_tmap(&tm_v);
-      mbar_expect_tx(&sm.bar_q, kTileBytes);
-      load_tile(&tm_q, &sm.bar_q, sm.q, h, j * 128);
+    // ------------------------------------------------------------ TMA producer (whole warp)
+    const uint32_t leader = elect_one();
+    if (n > 0) {
+      if (leader) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+      }
+      mbar_expect_tx_w(&sm.bar_q, kTileBytes, leader);
+      tma_load_3d_w(&tm_q, &sm.bar_q, sm.q, 0, h, j * 128, leader);
+      tma_load_3d_w(&tm_q, &sm.bar_q, sm.q + kTileBytes / 2, 64, h, j * 128, leader);
       for (int t = 0; t < n; ++t) {
         const int krow = p.k_row[tiles[t] >> 2] * 128;
         if (t > 0) mbar_wait(&sm.bar_k_empty, (t - 1) & 1);
-        mbar_expect_tx(&sm.bar_k_full, kTileBytes);
-        load_tile(&tm_k, &sm.bar_k_full, sm.k, hkv, krow);
+        mbar_expect_tx_w(&sm.bar_k_full, kTileBytes, leader);
+        tma_load_3d_w(&tm_k, &sm.bar_k_full, sm.k, 0, hkv, krow, leader);
+        tma_load_3d_w(&tm_k, &sm.bar_k_full, sm.k + kTileBytes / 2, 64, hkv, krow, leader);
         if (t > 0) mbar_wait(&sm.bar_v_empty, (t - 1) & 1);
-        mbar_expect_tx(&sm.bar_v_full, kTileBytes);
-        load_tile(&tm_v, &sm.bar_v_full, sm.v, hkv, krow);
+        mbar_expect_tx_w(&sm.bar_v_full, kTileBytes, leader);
+        tma_load_3d_w(&tm_v, &sm.bar_v_full, sm.v, 0, hkv, krow, leader);
+        tma_load_3d_w(&tm_v, &sm.bar_v_full, sm.v + kTileBytes / 2, 64, hkv, krow, leader);
       }
     }
   } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n > 0) {
+    // ------------------------------------------------------------ MMA issuer (whole warp)
+    const uint32_t leader = elect_one();
+    if (n > 0) {
       const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       const uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
-      const uint32_t sq = smem_u32(sm.q), sk = smem_u32(sm.k), sv = smem_u32(sm.v);
+      const uint64_t dq = sdesc_sw128(smem_u32(sm.q), 16, 1024);
+      const uint64_t dk = sdesc_sw128(smem_u32(sm.k), 16, 1024);
+      const uint64_t dv = sdesc_sw128(smem_u32(sm.v), kTileBytes / 2, 1024);
       mbar_wait(&sm.bar_q, 0);
       for (int t = 0; t < n; ++t) {
         mbar_wait(&sm.bar_k_full, t & 1);
@@ -106,138 +233,182 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-          mma_ss(tmem + kColS, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024),
-                 idesc_s, kk > 0);
+          const uint32_t off = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
+          mma_ss_w(tmem + kColS, dq + off, dk + off, idesc_s, kk > 0, leader);
         }
-        tc_commit(&sm.bar_s_full);
-        tc_commit(&sm.bar_k_empty);
+        tc_commit_w(&sm.bar_s_full, leader);
+        tc_commit_w(&sm.bar_k_empty, leader);
         mbar_wait(&sm.bar_p_full, t & 1);
         mbar_wait(&sm.bar_v_full, t & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + kColO, tmem + kColS + kk * 8,
-                 sdesc_sw128(sv + kk * 2048, kTileBytes / 2, 1024), idesc_o, (t > 0 || kk > 0));
-        tc_commit(&sm.bar_pv_done);
-        tc_commit(&sm.bar_v_empty);
+          mma_ts_w(tmem + kColO, tmem + kColS + kk * 8, dv + kk * 128, idesc_o, (t > 0 || kk > 0),
+                   leader);
+        tc_commit_w(&sm.bar_pv_done, leader);
+        tc_commit_w(&sm.bar_v_empty, leader);
       }
     }
   } else {
     // ------------------------------------------------------------ softmax warps 0-3
-    const int r = warp * 32 + lane;
-    const uint32_t lane_base = (warp * 32) << 16;
-    const long long qg = (long long)p.q_gid[j] * 128 + r;
-    const long long dq = p.desc[qg];
-    const float scale_log2 = p.scale * 1.4426950408889634f;
-    float m = -INFINITY, l = 0.f;
-    for (int t = 0; t < n; ++t) {
-      const int e = tiles[t];
-      const int cls = e & 3;
-      const long long kg0 = (long long)(e >> 2) * 128;
-      mbar_wait(&sm.bar_s_full, t & 1);
-      tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rr[32];
-        BAM_TMEM_LD32(tmem + lane_base + kColS + c * 32, rr);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(rr[i]);
-      }
-      if (cls == 2) {  // PARTIAL: descriptor predicate per element, 32 columns at a time
-        const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t bits = 0;
-#pragma unroll 4
-          for (int i = 0; i < 32; ++i) {
-            const long long d = __ldg(dk + c * 32 + i);
-            bits |= uint32_t(bam_allowed(dq, qg, d, kg0 + c * 32 + i)) << i;
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (!((bits >> i) & 1)) s[c * 32 + i] = -INFINITY;
-        }
-      }
-      float mt = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 128; ++c) mt = fmaxf(mt, s[c]);
-      const float m_new = fmaxf(m, mt * scale_log2);
-      // lazy rescale: only when the running max grows by more than 2^8
-      const bool rescale = m_new > m + 8.f;
-      const float alpha = rescale ? ex2(m - m_new) : 1.f;  // m = -inf -> 0
-      if (rescale) {
-        l *= alpha;
-        m = m_new;
-      }
-      const float mb = (m == -INFINITY) ? 0.f : m;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2(fmaf(s[c * 32 + 2 * i], scale_log2, -mb));
-          const float p1 = ex2(fmaf(s[c * 32 + 2 * i + 1], scale_log2, -mb));
-          l += p0 + p1;
-          pk[i] = pack_bf16(p0, p1);
-        }
-        BAM_TMEM_ST16(tmem + lane_base + kColS + c * 16, pk);
-      }
-      // warp-uniform branch: tcgen05.ld/st are .sync.aligned (alpha == 1 for rows that keep m)
-      if (__any_sync(0xffffffffu, rescale) && t > 0) {  // O(t-1) complete: S(t) issued after PV(t-1)
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t rr[32];
-          BAM_TMEM_LD32(tmem + lane_base + kColO + c * 32, rr);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
-          BAM_TMEM_ST32(tmem + lane_base + kColO + c * 32, rr);
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&sm.bar_p_full);
-    }
-    // epilogue: O / l -> bf16, LSE
-    const int64_t Tq = (int64_t)p.nq * 128;
-    const int64_t row = (int64_t)j * 128 + r;
-    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + (row * p.Hq + h) * 128;
-    if (n > 0) {
-      mbar_wait(&sm.bar_pv_done, (n - 1) & 1);
-      tc_fence_after();
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rr[32];
-        BAM_TMEM_LD32(tmem + lane_base + kColO + c * 32, rr);
-        tmem_wait_ld();
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(rr[8 * i + 0]) * inv, __uint_as_float(rr[8 * i + 1]) * inv);
-          v.y = pack_bf16(__uint_as_float(rr[8 * i + 2]) * inv, __uint_as_float(rr[8 * i + 3]) * inv);
-          v.z = pack_bf16(__uint_as_float(rr[8 * i + 4]) * inv, __uint_as_float(rr[8 * i + 5]) * inv);
-          v.w = pack_bf16(__uint_as_float(rr[8 * i + 6]) * inv, __uint_as_float(rr[8 * i + 7]) * inv);
-          dst[i] = v;
-        }
-      }
-      p.lse[(int64_t)h * Tq + row] =
-          l > 0.f ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
-    } else {
-      uint4* dst = reinterpret_cast<uint4*>(orow);
-      for (int i = 0; i < 16; ++i) dst[i] = make_uint4(0, 0, 0, 0);
-      p.lse[(int64_t)h * Tq + row] = -INFINITY;
-    }
+    softmax_role(p, tmem, kColS, kColO, &sm.bar_s_full, &sm.bar_p_full, &sm.bar_pv_done, j, h,
+                 warp, lane, tiles, n);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GQA head-pair kernel: one CTA = one 128-row query block x two query heads of
+// the same KV group (identical tile lists and masks, shared K/V tiles), 1 CTA
+// per SM.  TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).  The MMA
+// warp ping-pongs the two tiles so one warpgroup's softmax overlaps the other
+// tile's MMAs:  S0(0) S1(0) | PV0(0) S0(1) | PV1(0) S1(1) | PV0(1) S0(2) | ...
+// K/V tiles stream through a 2-stage ring.
+//   warps 0-3 softmax tile 0, warps 4-7 softmax tile 1, warp 8 TMA, warp 9 MMA.
+constexpr int kPairThreads = 320;
+
+struct PairSmem {
+  alignas(1024) uint8_t q[2][kTileBytes];
+  alignas(1024) uint8_t k[2][kTileBytes];
+  alignas(1024) uint8_t v[2][kTileBytes];
+  uint64_t bar_q, bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
+  uint64_t bar_s_full[2], bar_p_ready[2], bar_pv_done[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kPairThreads, 1)
+    attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int h0 = 2 * blockIdx.x;
+  const int j = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
+  const int hkv = h0 / (p.Hq / p.Hkv);
+  const int t0 = p.row_off[j], n = p.row_off[j + 1] - t0;
+  const int32_t* tiles = p.row_tiles + t0;
+
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B needs 1024-B alignment
+    mbar_init(&sm.bar_q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.bar_k_full[i], 1);
+      mbar_init(&sm.bar_k_empty[i], 1);
+      mbar_init(&sm.bar_v_full[i], 1);
+      mbar_init(&sm.bar_v_empty[i], 1);
+      mbar_init(&sm.bar_s_full[i], 1);
+      mbar_init(&sm.bar_p_ready[i], 128);
+      mbar_init(&sm.bar_pv_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer (whole warp)
+    const uint32_t leader = elect_one();
+    if (n > 0) {
+      if (leader) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+      }
+      mbar_expect_tx_w(&sm.bar_q, 2 * kTileBytes, leader);
+      for (int i = 0; i < 2; ++i) {
+        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i], 0, h0 + i, j * 128, leader);
+        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i] + kTileBytes / 2, 64, h0 + i, j * 128, leader);
+      }
+      for (int t = 0; t < n; ++t) {
+        const int st = t & 1;
+        const int krow = p.k_row[tiles[t] >> 2] * 128;
+        if (t >= 2) mbar_wait(&sm.bar_k_empty[st], ((t >> 1) - 1) & 1);
+        mbar_expect_tx_w(&sm.bar_k_full[st], kTileBytes, leader);
+        tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st], 0, hkv, krow, leader);
+        tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st] + kTileBytes / 2, 64, hkv, krow, leader);
+        if (t >= 2) mbar_wait(&sm.bar_v_empty[st], ((t >> 1) - 1) & 1);
+        mbar_expect_tx_w(&sm.bar_v_full[st], kTileBytes, leader);
+        tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st], 0, hkv, krow, leader);
+        tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st] + kTileBytes / 2, 64, hkv, krow, leader);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer (whole warp)
+    const uint32_t leader = elect_one();
+    if (n > 0) {
+      const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      const uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
+      const uint64_t dq0 = sdesc_sw128(smem_u32(sm.q[0]), 16, 1024);
+      const uint64_t dk0 = sdesc_sw128(smem_u32(sm.k[0]), 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(smem_u32(sm.v[0]), kTileBytes / 2, 1024);
+      constexpr uint32_t kTile16 = kTileBytes >> 4;
+      auto issue_s = [&](int i, int t) {  // S_i(t) = Q_i K(t)^T -> TMEM cols [128 i, +128)
+        const uint64_t dq = dq0 + i * kTile16, dk = dk0 + (t & 1) * kTile16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
+          mma_ss_w(tmem + 128 * i, dq + off, dk + off, idesc_s, kk > 0, leader);
+        }
+        tc_commit_w(&sm.bar_s_full[i], leader);
+      };
+      auto issue_pv = [&](int i, int t) {  // O_i += P_i(t) V(t), P_i bf16 in the S_i columns
+        const uint64_t dv = dv0 + (t & 1) * kTile16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts_w(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, dv + kk * 128, idesc_o,
+                   (t > 0 || kk > 0), leader);
+        tc_commit_w(&sm.bar_pv_done[i], leader);
+      };
+      mbar_wait(&sm.bar_q, 0);
+      mbar_wait(&sm.bar_k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      tc_commit_w(&sm.bar_k_empty[0], leader);
+      for (int t = 0; t < n; ++t) {
+        const int st = t & 1, st1 = (t + 1) & 1;
+        mbar_wait(&sm.bar_p_ready[0], t & 1);
+        mbar_wait(&sm.bar_v_full[st], (t >> 1) & 1);
+        tc_fence_after();
+        issue_pv(0, t);
+        if (t + 1 < n) {  // S0(t+1) overwrites P0(t): issued after PV0(t), executes in order
+          mbar_wait(&sm.bar_k_full[st1], ((t + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(0, t + 1);
+        }
+        mbar_wait(&sm.bar_p_ready[1], t & 1);
+        tc_fence_after();
+        issue_pv(1, t);
+        tc_commit_w(&sm.bar_v_empty[st], leader);
+        if (t + 1 < n) {
+          issue_s(1, t + 1);
+          tc_commit_w(&sm.bar_k_empty[st1], leader);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int i = warp >> 2;  // tile 0: warps 0-3, tile 1: warps 4-7
+    softmax_role(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i], &sm.bar_p_ready[i],
+                 &sm.bar_pv_done[i], j, h0 + i, warp, lane, tiles, n);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -259,11 +430,21 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
-  const int smem = (int)sizeof(fwd::Smem) + 1024;
-  BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid(p.Hq, p.nq);
-  fwd::attn_fwd_kernel<<<grid, fwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, p);
+  const int grp = p.Hq / p.Hkv;
+  if (grp % 2 == 0) {  // GQA: two query heads share each K/V tile
+    const int smem = (int)sizeof(fwd::PairSmem);
+    BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_pair_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid(p.Hq / 2, p.nq);
+    fwd::attn_fwd_pair_kernel<<<grid, fwd::kPairThreads, smem, (cudaStream_t)stream>>>(mq, mk,
+                                                                                       mv, p);
+  } else {
+    const int smem = (int)sizeof(fwd::Smem) + 1024;
+    BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    dim3 grid(p.Hq, p.nq);
+    fwd::attn_fwd_kernel<<<grid, fwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, p);
+  }
   BAM_LAUNCH_CHECK();
   return kOk;
 }
