@@ -159,7 +159,7 @@ typedef struct BamAttnBwdParams {
   const void* dout;         /* bf16 [nq*128, Hq, 128]             */
   const float* lse;         /* [Hq, nq*128] from the forward      */
   float* delta;             /* workspace [Hq, nq*128, 2]: (lse*log2e, rowsum(dO*O)) */
-  float* dq_acc;            /* workspace [nq*128, Hq, 128]        */
+  float* dq_acc;            /* workspace [Hq, nq*128, 128] fp32 (head-major) */
   void* dq;                 /* bf16 [nq*128, Hq, 128] out         */
   float* dk;                /* fp32 [k_rows*128, Hkv, 128] out    */
   float* dv;                /* fp32 [k_rows*128, Hkv, 128] out    */

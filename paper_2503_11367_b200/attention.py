@@ -141,7 +141,7 @@ def attn_backward(q, k, v, o, lse, do, plan: AttentionPlan, scale: float | None 
     Hq, Hkv = q.shape[1], k.shape[1]
     dev = q.device
     delta = torch.empty(Hq, q.shape[0], 2, dtype=torch.float32, device=dev)
-    dq_acc = torch.empty(q.shape, dtype=torch.float32, device=dev)
+    dq_acc = torch.empty(Hq, q.shape[0], 128, dtype=torch.float32, device=dev)
     dq = torch.empty_like(q)
     dk = torch.empty(k.shape, dtype=torch.float32, device=dev)
     dv = torch.empty(k.shape, dtype=torch.float32, device=dev)

@@ -56,16 +56,39 @@ __device__ __forceinline__ void red_add(float* addr, float a) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
 }
 
+// dst[(kRow0 + i) * 128] += v[i] for i < 32, rows 512 B apart (immediate offsets)
+template <int kRow0, int i = 0>
+__device__ __forceinline__ void red_add_rows(float* dst, const uint32_t (&v)[32]) {
+  if constexpr (i < 32) {
+    asm volatile("red.global.add.f32 [%0+%2], %1;" ::"l"(dst), "f"(__uint_as_float(v[i])),
+                 "n"((kRow0 + i) * 512)
+                 : "memory");
+    red_add_rows<kRow0, i + 1>(dst, v);
+  }
+}
+
 struct StepInfo {
   int h, jq, cls, half;
 };
 
-__device__ __forceinline__ StepInfo step_info(const int32_t* col, int s, int grp, int hkv) {
-  const int per_j = grp * 2;
-  const int e = col[s / per_j];
-  const int r = s % per_j;
-  return {hkv * grp + (r >> 1), e >> 2, e & 3, r & 1};
-}
+// Step s = (column entry s / (2 grp), head (s / 2) % grp, half s % 2), walked
+// incrementally (no integer division in the loops).
+struct StepIter {
+  const int32_t* col;
+  int per_j, h0, ci = 0, r = 0;
+  __device__ __forceinline__ StepIter(const int32_t* c, int grp, int hkv)
+      : col(c), per_j(2 * grp), h0(hkv * grp) {}
+  __device__ __forceinline__ StepInfo get() const {
+    const int e = col[ci];
+    return {h0 + (r >> 1), e >> 2, e & 3, r & 1};
+  }
+  __device__ __forceinline__ void next() {
+    if (++r == per_j) {
+      r = 0;
+      ++ci;
+    }
+  }
+};
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -123,11 +146,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_3d_w(&tm_k, &sm.bar_kv, sm.k + kTileBytes / 2, 64, hkv, krow0, leader);
       tma_load_3d_w(&tm_v, &sm.bar_kv, sm.v, 0, hkv, krow0, leader);
       tma_load_3d_w(&tm_v, &sm.bar_kv, sm.v + kTileBytes / 2, 64, hkv, krow0, leader);
+      StepIter it(col, grp, hkv);
       for (int s = 0; s < nsteps; ++s) {
         const int st = s % kStages;
-        const StepInfo si = step_info(col, s, grp, hkv);
+        const StepInfo si = it.get();
+        it.next();
         const int row0 = si.jq * 128 + si.half * 64;
-        if (s >= kStages) mbar_wait(&sm.bar_empty[st], ((s / kStages) - 1) & 1);
+        if (s >= kStages) mbar_wait_sleep(&sm.bar_empty[st], ((s / kStages) - 1) & 1);
         Stage& S = sm.st[st];
         mbar_expect_tx_w(&sm.bar_full[st], 2 * kHalfBytes + 512, leader);
         tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0, leader);
@@ -214,12 +239,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const long long kg = (long long)kb * 128 + r;
     const long long dk = p.desc[kg];
     const float scale_log2 = p.scale * 1.4426950408889634f;
+    StepIter it(col, grp, hkv);
     for (int s = 0; s < nsteps; ++s) {
       const int st = s % kStages, b = s & 1;
-      const StepInfo si = step_info(col, s, grp, hkv);
+      const StepInfo si = it.get();
+        it.next();
       const uint32_t tS = tmem + kColBuf + 128 * b + lane_base, tdP = tS + 64;
       const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
-      mbar_wait(&sm.bar_sdp_full[b], (s >> 1) & 1);
+      mbar_wait_sleep<32>(&sm.bar_sdp_full[b], (s >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
@@ -269,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* dvrow = p.dv + (row * p.Hkv + hkv) * 128;
     float* dkrow = p.dk + (row * p.Hkv + hkv) * 128;
     if (nsteps > 0) {
-      mbar_wait(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
+      mbar_wait_sleep(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -299,16 +326,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ dQ epilogue warps 4-7
-    // TMEM lane = head-dim column d; columns = the 64 queries of the step.
+    // TMEM lane = head-dim column d; columns = the 64 queries of the step.  The
+    // accumulator is head-major [Hq, rows, 128] fp32, so the 64 rows of a step
+    // sit at compile-time 512-B strides from one base (immediate offsets).
     const int d = (warp - 4) * 32 + lane;
     const uint32_t lane_base = ((warp - 4) * 32) << 16;
+    StepIter it(col, grp, hkv);
     for (int s = 0; s < nsteps; ++s) {
       const int b = s & 1;
-      const StepInfo si = step_info(col, s, grp, hkv);
-      float* dst = p.dq_acc + ((int64_t)(si.jq * 128 + si.half * 64) * p.Hq + si.h) * 128 + d;
-      const int64_t qstride = (int64_t)p.Hq * 128;
+      const StepInfo si = it.get();
+        it.next();
+      float* dst = p.dq_acc + ((int64_t)si.h * Tq + si.jq * 128 + si.half * 64) * 128 + d;
       const uint32_t tDQ = tmem + kColBuf + 128 * b + 64;
-      mbar_wait(&sm.bar_dq_full[b], (s >> 1) & 1);
+      mbar_wait_sleep(&sm.bar_dq_full[b], (s >> 1) & 1);
       tc_fence_after();
       uint32_t a[32], c2[32];
       BAM_TMEM_LD32(tDQ + lane_base, a);
@@ -320,16 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (a[0] == 0x7fc00001u) red_add(dst, 1.f);   // keep the loads live, skip the reductions
       continue;
 #endif
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        red_add(dst, __uint_as_float(a[i]));
-        dst += qstride;
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        red_add(dst, __uint_as_float(c2[i]));
-        dst += qstride;
-      }
+      red_add_rows<0>(dst, a);
+      red_add_rows<32>(dst, c2);
     }
   }
   tc_fence_before();
@@ -366,13 +388,16 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
   }
 }
 
-// dq (bf16) = dq_acc * scale
-__global__ void bwd_dq_convert_kernel(const float4* __restrict__ acc, uint2* __restrict__ dq,
-                                      int64_t n4, float scale) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = acc[i];
-    dq[i] = make_uint2(pack_bf16(v.x * scale, v.y * scale), pack_bf16(v.z * scale, v.w * scale));
+// dq[row, h, :] (bf16) = scale * dq_acc[h, row, :]   (one warp per (row, h))
+__global__ void bwd_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
+                                      int64_t rows, int H, float scale) {
+  const int64_t nw = rows * H;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t row = w / H, h = w % H;
+    const float4 v = reinterpret_cast<const float4*>(acc + (h * rows + row) * 128)[lane_id()];
+    reinterpret_cast<uint2*>(dq + w * 128)[lane_id()] =
+        make_uint2(pack_bf16(v.x * scale, v.y * scale), pack_bf16(v.z * scale, v.w * scale));
   }
 }
 
@@ -429,9 +454,8 @@ int bam_attn_bwd_main(const BamAttnBwdParams* pp, void* stream) {
 int bam_attn_bwd_finalize(const BamAttnBwdParams* pp, void* stream) {
   if (int rc = check_bwd(pp)) return rc;
   const BamAttnBwdParams& p = *pp;
-  const int64_t n4 = (int64_t)p.nq * 128 * p.Hq * 32;
   bwd::bwd_dq_convert_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const float4*>(p.dq_acc), reinterpret_cast<uint2*>(p.dq), n4, p.scale);
+      p.dq_acc, reinterpret_cast<__nv_bfloat16*>(p.dq), (int64_t)p.nq * 128, p.Hq, p.scale);
   BAM_LAUNCH_CHECK();
   return kOk;
 }

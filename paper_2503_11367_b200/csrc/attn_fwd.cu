@@ -61,7 +61,7 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
     const int e = tiles[t];
     const int cls = e & 3;
     const long long kg0 = (long long)(e >> 2) * 128;
-    mbar_wait(bar_s_full, t & 1);
+    mbar_wait_sleep<32>(bar_s_full, t & 1);
     tc_fence_after();
     float s[128];
 #pragma unroll
@@ -133,7 +133,7 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
   const int64_t row = (int64_t)j * 128 + r;
   __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + (row * p.Hq + h) * 128;
   if (n > 0) {
-    mbar_wait(bar_pv_done, (n - 1) & 1);
+    mbar_wait_sleep(bar_pv_done, (n - 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
@@ -207,11 +207,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       tma_load_3d_w(&tm_q, &sm.bar_q, sm.q + kTileBytes / 2, 64, h, j * 128, leader);
       for (int t = 0; t < n; ++t) {
         const int krow = p.k_row[tiles[t] >> 2] * 128;
-        if (t > 0) mbar_wait(&sm.bar_k_empty, (t - 1) & 1);
+        if (t > 0) mbar_wait_sleep(&sm.bar_k_empty, (t - 1) & 1);
         mbar_expect_tx_w(&sm.bar_k_full, kTileBytes, leader);
         tma_load_3d_w(&tm_k, &sm.bar_k_full, sm.k, 0, hkv, krow, leader);
         tma_load_3d_w(&tm_k, &sm.bar_k_full, sm.k + kTileBytes / 2, 64, hkv, krow, leader);
-        if (t > 0) mbar_wait(&sm.bar_v_empty, (t - 1) & 1);
+        if (t > 0) mbar_wait_sleep(&sm.bar_v_empty, (t - 1) & 1);
         mbar_expect_tx_w(&sm.bar_v_full, kTileBytes, leader);
         tma_load_3d_w(&tm_v, &sm.bar_v_full, sm.v, 0, hkv, krow, leader);
         tma_load_3d_w(&tm_v, &sm.bar_v_full, sm.v + kTileBytes / 2, 64, hkv, krow, leader);
@@ -334,11 +334,11 @@ __global__ void __launch_bounds__(kPairThreads, 1)
       for (int t = 0; t < n; ++t) {
         const int st = t & 1;
         const int krow = p.k_row[tiles[t] >> 2] * 128;
-        if (t >= 2) mbar_wait(&sm.bar_k_empty[st], ((t >> 1) - 1) & 1);
+        if (t >= 2) mbar_wait_sleep(&sm.bar_k_empty[st], ((t >> 1) - 1) & 1);
         mbar_expect_tx_w(&sm.bar_k_full[st], kTileBytes, leader);
         tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st], 0, hkv, krow, leader);
         tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st] + kTileBytes / 2, 64, hkv, krow, leader);
-        if (t >= 2) mbar_wait(&sm.bar_v_empty[st], ((t >> 1) - 1) & 1);
+        if (t >= 2) mbar_wait_sleep(&sm.bar_v_empty[st], ((t >> 1) - 1) & 1);
         mbar_expect_tx_w(&sm.bar_v_full[st], kTileBytes, leader);
         tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st], 0, hkv, krow, leader);
         tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st] + kTileBytes / 2, 64, hkv, krow, leader);

@@ -88,24 +88,35 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, 1000000;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, P;\n\t}\n"
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
   return ok;
 }
-// Bounded wait: a protocol bug traps (a reported launch failure) instead of
-// hanging the GPU.  ~20 s at 2 GHz.
+// Bounded waits: a protocol bug traps (a reported launch failure) instead of
+// hanging the GPU.  mbar_wait spins tightly (latency-critical roles: the MMA
+// issuer); mbar_wait_sleep backs off with nanosleep so waiting warps do not
+// steal issue slots from the warps sharing their SM sub-partition.
+static __device__ __noinline__ void mbar_timeout_trap() {
+  printf("bam: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+  __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  if (mbar_try_wait(addr, parity)) return;
-  const long long t0 = clock64();
+  uint32_t iters = 0;
   while (!mbar_try_wait(addr, parity)) {
-    if (clock64() - t0 > 40000000000LL) {
-      printf("bam: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
-      __trap();
-    }
+    if (++iters > (1u << 28)) mbar_timeout_trap();
+  }
+}
+template <int kSleepNs = 64>
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t iters = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    __nanosleep(kSleepNs);
+    if (++iters > (1u << 28)) mbar_timeout_trap();
   }
 }
 
