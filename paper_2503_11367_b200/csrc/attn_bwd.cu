@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         it.next();
       const uint32_t tS = tmem + kColBuf + 128 * b + lane_base, tdP = tS + 64;
       const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
-      mbar_wait_sleep<32>(&sm.bar_sdp_full[b], (s >> 1) & 1);
+      mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_sdp_full[b], (s >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {

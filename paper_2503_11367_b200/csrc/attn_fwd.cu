@@ -61,7 +61,7 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
     const int e = tiles[t];
     const int cls = e & 3;
     const long long kg0 = (long long)(e >> 2) * 128;
-    mbar_wait_sleep<32>(bar_s_full, t & 1);
+    mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(bar_s_full, t & 1);
     tc_fence_after();
     float s[128];
 #pragma unroll

@@ -115,10 +115,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   const uint32_t addr = smem_u32(bar);
   uint32_t iters = 0;
   while (!mbar_try_wait(addr, parity)) {
-    __nanosleep(kSleepNs);
+    if constexpr (kSleepNs > 0) __nanosleep(kSleepNs);
     if (++iters > (1u << 28)) mbar_timeout_trap();
   }
 }
+
+#ifndef BAM_COMPUTE_SLEEP_NS
+#define BAM_COMPUTE_SLEEP_NS 32   // back-off of the softmax / compute warps' waits
+#endif
 
 // ----------------------------------------------------------------------------- TMA
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
