@@ -18,10 +18,10 @@
 // TMEM lanes, so the dQ warps' fp32 reductions into dq_acc are coalesced
 // (one 128-B row segment per warp instruction).
 // Q/dO half tiles stream through a 4-stage TMA ring.
-// Warp roles (320 threads, 1 CTA / SM):
-//   warps 0-3 compute (thread r = key row r), warps 4-7 dQ epilogue
-//   (thread r = head-dim column r), warp 8 MMA issuer + TMEM alloc,
-//   warp 9 TMA producer (Q/dO half tiles + LSE/D pairs).
+// Warp roles (448 threads, 1 CTA / SM):
+//   warps 0-7 compute (two warpgroups, 32 query columns each; thread r = key
+//   row r), warps 8-11 dQ epilogue (thread r = head-dim column r), warp 12
+//   MMA issuer + TMEM alloc, warp 13 TMA producer (Q/dO half tiles + LSE/D).
 #include "../../include/bam.h"
 #include "common.cuh"
 #include "tma.h"
@@ -29,7 +29,9 @@
 namespace bam {
 namespace bwd {
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;
+// warp roles
+constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
 constexpr int kStages = 4;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
 constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
@@ -115,14 +117,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.bar_sdp_full[b], 1);
-      mbar_init(&sm.bar_p_ready[b], 128);
+      mbar_init(&sm.bar_p_ready[b], 256);
       mbar_init(&sm.bar_mma_done[b], 1);
       mbar_init(&sm.bar_dq_full[b], 1);
       mbar_init(&sm.bar_dq_empty[b], 128);
     }
     fence_mbar_init();
   }
-  if (warp == 8) {
+  if (warp == kWarpMMA) {
     tmem_alloc(&sm.tmem_base, 512);
     tmem_relinquish();
   }
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 9) {
+  if (warp == kWarpTMA) {
     // ------------------------------------------------------------ TMA producer (whole warp)
     const uint32_t leader = elect_one();
     if (nsteps > 0) {
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     leader);
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == kWarpMMA) {
     // ------------------------------------------------------------ MMA issuer (whole warp)
     // Descriptors are built once; per MMA only the 14-bit start-address field
     // advances (adding offset >> 4 to the 64-bit descriptor cannot carry out).
@@ -232,10 +234,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit_w(&sm.bar_mma_done[b], leader);
       }
     }
-  } else if (warp < 4) {
-    // ------------------------------------------------------------ compute warps 0-3
-    const int r = warp * 32 + lane;
-    const uint32_t lane_base = (warp * 32) << 16;
+  } else if (warp < kWarpDQ) {
+    // ------------------------------------------------------------ compute warps 0-7
+    // Two warpgroups split the 64 queries of a step: warpgroup c takes query
+    // columns [32c, 32c+32); thread r = key row r = TMEM lane r in both.
+    const int c = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = ((warp & 3) * 32) << 16;
     const long long kg = (long long)kb * 128 + r;
     const long long dk = p.desc[kg];
     const float scale_log2 = p.scale * 1.4426950408889634f;
@@ -243,94 +248,81 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < nsteps; ++s) {
       const int st = s % kStages, b = s & 1;
       const StepInfo si = it.get();
-        it.next();
+      it.next();
       const uint32_t tS = tmem + kColBuf + 128 * b + lane_base, tdP = tS + 64;
       const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
       mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_sdp_full[b], (s >> 1) & 1);
       tc_fence_after();
+      uint32_t sr[32], dr[32];
+      BAM_TMEM_LD32(tS + c * 32, sr);
+      BAM_TMEM_LD32(tdP + c * 32, dr);
+      uint32_t allow = 0xFFFFFFFFu;
+      if (si.cls == 2) {  // PARTIAL tile: descriptor predicate for these 32 queries
+        const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64 + c * 32;
+        allow = 0;
 #pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t sr[32], dr[32];
-        BAM_TMEM_LD32(tS + c * 32, sr);
-        BAM_TMEM_LD32(tdP + c * 32, dr);
-        uint32_t allow = 0xFFFFFFFFu;
-        if (si.cls == 2) {  // PARTIAL tile: descriptor predicate for these 32 queries
-          const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64 + c * 32;
-          allow = 0;
-#pragma unroll 1
-          for (int i = 0; i < 32; ++i)
-            allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
-        }
-        tmem_wait_ld();
-        const float4* ld = reinterpret_cast<const float4*>(sm.ld[st] + c * 64);  // (lse*log2e, D)
-        uint32_t pk[16], dsk[16];
+        for (int i = 0; i < 32; ++i)
+          allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
+      }
+      tmem_wait_ld();
+      const float4* ld = reinterpret_cast<const float4*>(sm.ld[st] + c * 64);  // (lse*log2e, D)
+      uint32_t pk[16], dsk[16];
 #pragma unroll
-        for (int i2 = 0; i2 < 16; ++i2) {
-          const float4 v = ld[i2];
-          float p0 = ex2(fmaf(__uint_as_float(sr[2 * i2]), scale_log2, -v.x));
-          float p1 = ex2(fmaf(__uint_as_float(sr[2 * i2 + 1]), scale_log2, -v.z));
-          p0 = (allow >> (2 * i2)) & 1 ? p0 : 0.f;
-          p1 = (allow >> (2 * i2 + 1)) & 1 ? p1 : 0.f;
-          pk[i2] = pack_bf16(p0, p1);
-          dsk[i2] = pack_bf16(p0 * (__uint_as_float(dr[2 * i2]) - v.y),
-                              p1 * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
-        }
-        BAM_TMEM_ST16(tS + c * 16, pk);
-        // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
+      for (int i2 = 0; i2 < 16; ++i2) {
+        const float4 v = ld[i2];
+        float p0 = ex2(fmaf(__uint_as_float(sr[2 * i2]), scale_log2, -v.x));
+        float p1 = ex2(fmaf(__uint_as_float(sr[2 * i2 + 1]), scale_log2, -v.z));
+        p0 = (allow >> (2 * i2)) & 1 ? p0 : 0.f;
+        p1 = (allow >> (2 * i2 + 1)) & 1 ? p1 : 0.f;
+        pk[i2] = pack_bf16(p0, p1);
+        dsk[i2] = pack_bf16(p0 * (__uint_as_float(dr[2 * i2]) - v.y),
+                            p1 * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
+      }
+      BAM_TMEM_ST16(tS + c * 16, pk);
+      // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t chunk = (uint32_t)(c * 4 + q4) ^ (uint32_t)(r & 7);
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ds_row + chunk * 16),
-                       "r"(dsk[q4 * 4]), "r"(dsk[q4 * 4 + 1]), "r"(dsk[q4 * 4 + 2]),
-                       "r"(dsk[q4 * 4 + 3])
-                       : "memory");
-        }
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint32_t chunk = (uint32_t)(c * 4 + q4) ^ (uint32_t)(r & 7);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ds_row + chunk * 16),
+                     "r"(dsk[q4 * 4]), "r"(dsk[q4 * 4 + 1]), "r"(dsk[q4 * 4 + 2]),
+                     "r"(dsk[q4 * 4 + 3])
+                     : "memory");
       }
       tmem_wait_st();
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&sm.bar_p_ready[b]);
     }
-    // epilogue: dV, dK (scaled) -> fp32 rows of the key block
+    // epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled), fp32 rows
     const int64_t row = (int64_t)krow0 + r;
-    float* dvrow = p.dv + (row * p.Hkv + hkv) * 128;
-    float* dkrow = p.dk + (row * p.Hkv + hkv) * 128;
+    float* dst = (c == 0 ? p.dv : p.dk) + (row * p.Hkv + hkv) * 128;
+    const float mul = c == 0 ? 1.f : p.scale;
     if (nsteps > 0) {
       mbar_wait_sleep(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t a[32], bb[32];
-        BAM_TMEM_LD32(tmem + lane_base + kColDV + c * 32, a);
-        BAM_TMEM_LD32(tmem + lane_base + kColDK + c * 32, bb);
+      for (int q = 0; q < 4; ++q) {
+        uint32_t a[32];
+        BAM_TMEM_LD32(tmem + lane_base + (c == 0 ? kColDV : kColDK) + q * 32, a);
         tmem_wait_ld();
-        float4* dv4 = reinterpret_cast<float4*>(dvrow + c * 32);
-        float4* dk4 = reinterpret_cast<float4*>(dkrow + c * 32);
+        float4* d4 = reinterpret_cast<float4*>(dst + q * 32);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          dv4[i] = make_float4(__uint_as_float(a[4 * i]), __uint_as_float(a[4 * i + 1]),
-                               __uint_as_float(a[4 * i + 2]), __uint_as_float(a[4 * i + 3]));
-          dk4[i] = make_float4(__uint_as_float(bb[4 * i]) * p.scale,
-                               __uint_as_float(bb[4 * i + 1]) * p.scale,
-                               __uint_as_float(bb[4 * i + 2]) * p.scale,
-                               __uint_as_float(bb[4 * i + 3]) * p.scale);
-        }
+        for (int i = 0; i < 8; ++i)
+          d4[i] = make_float4(__uint_as_float(a[4 * i]) * mul, __uint_as_float(a[4 * i + 1]) * mul,
+                              __uint_as_float(a[4 * i + 2]) * mul,
+                              __uint_as_float(a[4 * i + 3]) * mul);
       }
     } else {
-      float4* dv4 = reinterpret_cast<float4*>(dvrow);
-      float4* dk4 = reinterpret_cast<float4*>(dkrow);
-      for (int i = 0; i < 32; ++i) {
-        dv4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        dk4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      float4* d4 = reinterpret_cast<float4*>(dst);
+      for (int i = 0; i < 32; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   } else {
-    // ------------------------------------------------------------ dQ epilogue warps 4-7
+    // ------------------------------------------------------------ dQ epilogue warps 8-11
     // TMEM lane = head-dim column d; columns = the 64 queries of the step.  The
     // accumulator is head-major [Hq, rows, 128] fp32, so the 64 rows of a step
     // sit at compile-time 512-B strides from one base (immediate offsets).
-    const int d = (warp - 4) * 32 + lane;
-    const uint32_t lane_base = ((warp - 4) * 32) << 16;
+    const int d = (warp - kWarpDQ) * 32 + lane;
+    const uint32_t lane_base = ((warp - kWarpDQ) * 32) << 16;
     StepIter it(col, grp, hkv);
     for (int s = 0; s < nsteps; ++s) {
       const int b = s & 1;
@@ -356,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kWarpMMA) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
