@@ -190,6 +190,10 @@ int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 int bam_selftest_umma(const void* a, const void* b, const void* v, const void* x, float* out,
                       void* stream);
 
+/* Development aid: install a device buffer ([events][4096] u64 clock64 stamps
+ * of one CTA) for -DBAM_TRACE builds; BAM_UNSUPPORTED in normal builds. */
+int bam_set_trace_buffer(void* buf);
+
 #ifdef __cplusplus
 }
 #endif

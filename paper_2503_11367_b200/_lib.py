@@ -66,6 +66,7 @@ SIGNATURES = {
     "bam_attn_bwd_finalize": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "bam_selftest_umma": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bam_set_trace_buffer": (c_i32, [c_vp]),
 }
 
 BAM_OK, BAM_INVALID_ARGUMENT, BAM_CUDA_ERROR, BAM_UNSUPPORTED, BAM_BUDGET_EXCEEDED = range(5)

@@ -107,6 +107,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nsteps = ncol * grp * 2;
   const int64_t Tq = (int64_t)p.nq * 128;
   const int krow0 = p.k_row[kb] * 128;
+  const bool trace_cta = blockIdx.x == 0 && blockIdx.y == 0;
+  (void)trace_cta;
+#ifdef BAM_TRACE
+  unsigned long long* const bam_trace_ptr = trace_cta ? g_bam_trace : nullptr;
+#endif
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B needs 1024-B alignment
@@ -155,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         it.next();
         const int row0 = si.jq * 128 + si.half * 64;
         if (s >= kStages) mbar_wait_sleep(&sm.bar_empty[st], ((s / kStages) - 1) & 1);
+        BAM_TRACE_EV(trace_cta && leader, 10, s);
         Stage& S = sm.st[st];
         mbar_expect_tx_w(&sm.bar_full[st], 2 * kHalfBytes + 512, leader);
         tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0, leader);
@@ -185,18 +191,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_sdp = [&](int s) {
         const int st = s % kStages, b = s & 1;
         mbar_wait(&sm.bar_full[st], (s / kStages) & 1);
+        BAM_TRACE_EV(trace_cta && leader, 11, s);
         // S_b still holds P^T(s-2), read by dV(s-2): issued earlier by this warp, and
         // tcgen05.mma ops from one thread execute in issue order, so no wait is needed.
         tc_fence_after();
+        BAM_TRACE_EV(trace_cta && leader, 16, s);
         const uint32_t tS = tmem + kColBuf + 128 * b, tdP = tS + 64;
         const uint64_t dq = d_q0 + st * kStage16, ddo = dq + kDo16;
+        BAM_TRACE_EV(trace_cta && leader, 0, s);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t ka = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
           const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
           mma_ss_w(tS, dk_k + ka, dq + kq, id_s, kk > 0, leader);
         }
+        BAM_TRACE_EV(trace_cta && leader, 12, s);
         if (s >= 2) mbar_wait(&sm.bar_dq_empty[b], ((s >> 1) - 1) & 1);  // dQ^T(s-2) drained
+        BAM_TRACE_EV(trace_cta && leader, 1, s);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -205,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ss_w(tdP, dk_v + ka, ddo + kq, id_s, kk > 0, leader);
         }
         tc_commit_w(&sm.bar_sdp_full[b], leader);
+        BAM_TRACE_EV(trace_cta && leader, 13, s);
       };
       mbar_wait(&sm.bar_kv, 0);
       issue_sdp(0);
@@ -215,15 +227,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dds = d_ds0 + b * kDs16;
         const uint32_t tS = tmem + kColBuf + 128 * b, tDQ = tS + 64;
         mbar_wait(&sm.bar_p_ready[b], (s >> 1) & 1);
+        BAM_TRACE_EV(trace_cta && leader, 2, s);
         tc_fence_after();
         // dV += P^T dO   (K = 64 queries: 4 steps of 16 rows = 2048 B)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           mma_ts_w(tmem + kColDV, tS + kk * 8, ddomn + kk * 128, id_kv, (s > 0 || kk > 0), leader);
+        BAM_TRACE_EV(trace_cta && leader, 14, s);
         // dK += dS^T Q   (dS^T K-major: 32 B per 16 queries)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           mma_ss_w(tmem + kColDK, dds + kk * 2, dqmn + kk * 128, id_kv, (s > 0 || kk > 0), leader);
+        BAM_TRACE_EV(trace_cta && leader, 15, s);
         // dQ^T = K^T dS^T  (K = 128 keys: 8 steps of 16 key rows = 2048 B); dS^T as MN-major
         // B uses the same start address with LBO unused (N = 64 = one swizzle atom)
 #pragma unroll
@@ -232,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit_w(&sm.bar_dq_full[b], leader);
         tc_commit_w(&sm.bar_empty[st], leader);
         tc_commit_w(&sm.bar_mma_done[b], leader);
+        BAM_TRACE_EV(trace_cta && leader, 3, s);
       }
     }
   } else if (warp < kWarpDQ) {
@@ -252,6 +268,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tS = tmem + kColBuf + 128 * b + lane_base, tdP = tS + 64;
       const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
       mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_sdp_full[b], (s >> 1) & 1);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 4, s);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 128, 6, s);
       tc_fence_after();
       uint32_t sr[32], dr[32];
       BAM_TMEM_LD32(tS + c * 32, sr);
@@ -265,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
       }
       tmem_wait_ld();
+      BAM_TRACE_EV(threadIdx.x == 0, 17, s);
       const float4* ld = reinterpret_cast<const float4*>(sm.ld[st] + c * 64);  // (lse*log2e, D)
       uint32_t pk[16], dsk[16];
 #pragma unroll
@@ -278,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         dsk[i2] = pack_bf16(p0 * (__uint_as_float(dr[2 * i2]) - v.y),
                             p1 * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
       }
+      BAM_TRACE_EV(threadIdx.x == 0, 18, s);
       BAM_TMEM_ST16(tS + c * 16, pk);
       // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
 #pragma unroll
@@ -289,8 +309,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                      : "memory");
       }
       tmem_wait_st();
+      BAM_TRACE_EV(threadIdx.x == 0, 19, s);
       fence_async_smem();
       tc_fence_before();
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 5, s);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 128, 7, s);
       mbar_arrive(&sm.bar_p_ready[b]);
     }
     // epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled), fp32 rows
@@ -331,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* dst = p.dq_acc + ((int64_t)si.h * Tq + si.jq * 128 + si.half * 64) * 128 + d;
       const uint32_t tDQ = tmem + kColBuf + 128 * b + 64;
       mbar_wait_sleep(&sm.bar_dq_full[b], (s >> 1) & 1);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == kWarpDQ * 32, 8, s);
       tc_fence_after();
       uint32_t a[32], c2[32];
       BAM_TMEM_LD32(tDQ + lane_base, a);
@@ -344,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       red_add_rows<0>(dst, a);
       red_add_rows<32>(dst, c2);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == kWarpDQ * 32, 9, s);
     }
   }
   tc_fence_before();
@@ -410,6 +435,19 @@ static int check_bwd(const BamAttnBwdParams* pp) {
 }
 
 extern "C" {
+
+// Development aid: install the per-step trace buffer of -DBAM_TRACE builds of
+// the backward kernel (returns BAM_UNSUPPORTED otherwise).
+int bam_set_trace_buffer(void* buf) {
+#ifdef BAM_TRACE
+  BAM_CUDA_TRY(cudaMemcpyToSymbol(g_bam_trace, &buf, sizeof(buf)));
+  return BAM_OK;
+#else
+  (void)buf;
+  set_last_error("libbam built without -DBAM_TRACE");
+  return BAM_UNSUPPORTED;
+#endif
+}
 
 int bam_attn_bwd_preprocess(const BamAttnBwdParams* pp, void* stream) {
   if (int rc = check_bwd(pp)) return rc;

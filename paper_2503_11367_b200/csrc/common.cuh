@@ -124,6 +124,24 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 #define BAM_COMPUTE_SLEEP_NS 32   // back-off of the softmax / compute warps' waits
 #endif
 
+// ----------------------------------------------------------------------------- tracing
+// -DBAM_TRACE builds record clock64() per (event, step) for one CTA into a
+// device buffer installed with bam_set_trace_buffer (development aid).
+#ifdef BAM_TRACE
+constexpr int kTraceSteps = 4096;
+static __device__ unsigned long long* g_bam_trace = nullptr;   // per translation unit
+// kernels load the pointer once: unsigned long long* const bam_trace_ptr = g_bam_trace;
+#define BAM_TRACE_EV(cond, ev, step)                                                 \
+  do {                                                                               \
+    if ((cond) && bam_trace_ptr && (step) < ::bam::kTraceSteps)                      \
+      bam_trace_ptr[(ev) * ::bam::kTraceSteps + (step)] = clock64();                 \
+  } while (0)
+#else
+#define BAM_TRACE_EV(cond, ev, step) \
+  do {                               \
+  } while (0)
+#endif
+
 // ----------------------------------------------------------------------------- TMA
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

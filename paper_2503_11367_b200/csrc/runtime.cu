@@ -78,6 +78,7 @@ using namespace bam;
 extern "C" {
 
 const char* bam_last_error(void) { return g_last_error; }
+
 int bam_version(void) { return 1; }
 
 int bam_ilp_optimal(const int64_t* w, int32_t n, int32_t G, int32_t* assignment,
