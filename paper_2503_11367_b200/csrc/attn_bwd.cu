@@ -8,6 +8,7 @@
 // (j outer, head, half inner, so CTAs running together hit the same dQ
 // accumulator lines in L2):
 //   S^T  = K Q^T      (SS, M=128 keys, N=64)  -> TMEM S_b      P^T = exp2(S^T c - LSE)
+//                     (P^T bf16 of queries [32c, 32c+32) over S_b cols [32c, 32c+16))
 //   dP^T = V dO^T     (SS)                    -> TMEM dP_b     dS^T = P^T (dP^T - D)
 //   dV  += P^T dO     (TS: P^T bf16 in S_b, dO MN-major)       -> TMEM [0,128)
 //   dK  += dS^T Q     (SS: dS^T smem K-major, Q MN-major)      -> TMEM [128,256)
@@ -231,8 +232,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         // dV += P^T dO   (K = 64 queries: 4 steps of 16 rows = 2048 B)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ts_w(tmem + kColDV, tS + kk * 8, ddomn + kk * 128, id_kv, (s > 0 || kk > 0), leader);
+        for (int kk = 0; kk < 4; ++kk)  // P^T for queries [16kk, 16kk+16) at TMEM col 32(kk>>1)+8(kk&1)
+          mma_ts_w(tmem + kColDV, tS + (kk >> 1) * 32 + (kk & 1) * 8, ddomn + kk * 128, id_kv,
+                   (s > 0 || kk > 0), leader);
         BAM_TRACE_EV(trace_cta && leader, 14, s);
         // dK += dS^T Q   (dS^T K-major: 32 B per 16 queries)
 #pragma unroll
@@ -298,7 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             p1 * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
       }
       BAM_TRACE_EV(threadIdx.x == 0, 18, s);
-      BAM_TMEM_ST16(tS + c * 16, pk);
+      // P^T (bf16 pairs) goes over the S columns this warpgroup itself read,
+      // [32c, 32c+16): the other warpgroup may still be loading its own columns.
+      BAM_TMEM_ST16(tS + c * 32, pk);
       // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
