@@ -142,3 +142,31 @@ def test_autograd_function():
     assert_close("dQ", qd.grad, q_g)
     assert_close("dK", kd.grad, k_g)
     assert_close("dV", vd.grad, v_g)
+
+
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_repeat_bitwise_deterministic(cfg_id):
+    """Race detector: O, LSE, dK, dV have no atomics, so repeated runs on the
+    same inputs must agree bit for bit (dQ uses fp32 reductions and may not)."""
+    from paper_2503_11367_b200 import attention as A, mask as M
+    from paper_2503_11367_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[cfg_id]
+    mask = M.build_bitfield(cfg["segments"])
+    plan = A.plan_for_mask(mask)
+    T, dev = len(mask), torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(99)
+    q = torch.randn(T, cfg["Hq"], 128, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(T, cfg["Hkv"], 128, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(T, cfg["Hkv"], 128, device=dev, generator=g, dtype=torch.bfloat16)
+    do = torch.randn(T, cfg["Hq"], 128, device=dev, generator=g, dtype=torch.bfloat16)
+    ref = None
+    for _ in range(3):
+        o, lse = A.attn_forward(q, k, v, plan)
+        _, dk, dv = A.attn_backward(q, k, v, o, lse, do, plan, dkv_fp32=True)
+        cur = [t.clone() for t in (o, lse, dk, dv)]
+        if ref is None:
+            ref = cur
+        else:
+            for name, a, b in zip(("O", "LSE", "dK", "dV"), cur, ref):
+                assert torch.equal(a, b), f"{name} differs between identical runs (race?)"
