@@ -319,6 +319,14 @@ def main():
     e2e_value = flop_step / (e2e_ms * 1e-3) / 1e12
 
     peaks, peak_src = load_peaks()
+    traffic = None
+    try:   # DRAM bytes per launch from the committed ncu --set full capture (N=1 only)
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as fh:
+            tr = json.load(fh).get(cfg["name"], {}).get("attn_bwd_kernel")
+        if tr and world == tr["n_gpus"]:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     peak = peaks["bf16_tflops"]
     bwd_achieved = flop_local_bwd / (bwd_main_ms * 1e-3) / 1e12
     fwd_achieved = flop_local_fwd / (fwd_ms * 1e-3) / 1e12
@@ -350,7 +358,8 @@ def main():
             "imbalance_predicted": imb_pred, "imbalance_measured": imb_meas,
             "roofline": {"bound": "tensor", "kernel": "bam attn_bwd_kernel (tcgen05)",
                          "achieved": bwd_achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": bwd_achieved / peak, "traffic": None,
+                         "frac": bwd_achieved / peak, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per launch (ncu capture, profiles/r01)",
                          "peak_source": peak_src + " bf16_tflops (burst)",
                          "fwd": {"kernel": "bam attn_fwd_kernel", "achieved": fwd_achieved,
                                  "frac": fwd_achieved / peak}},
