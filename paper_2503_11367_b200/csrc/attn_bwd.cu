@@ -33,7 +33,12 @@ namespace bwd {
 constexpr int kThreads = 448;
 // warp roles
 constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
-constexpr int kStages = 4;
+// dQ^T tiles leave through one 32-KB TMA bulk reduce-add per step (staged in
+// shared memory) instead of 64 per-thread reductions; costs one Q/dO stage.
+#ifndef BAM_DQ_BULK
+#define BAM_DQ_BULK 1
+#endif
+constexpr int kStages = BAM_DQ_BULK ? 3 : 4;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
 constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
 constexpr uint32_t kDsBytes = 128 * 64 * 2;      // dS^T: 128 key rows x 64 query cols
@@ -49,6 +54,9 @@ struct Smem {
   alignas(1024) uint8_t v[kTileBytes];
   alignas(1024) uint8_t ds[2][kDsBytes];
   Stage st[kStages];
+#if BAM_DQ_BULK
+  alignas(128) float dq_stage[64 * 128];  // dQ tile [64 queries][128 d] fp32 for the bulk reduce
+#endif
   alignas(16) float ld[kStages][128];   // per stage: (lse * log2e, delta) pairs, 64 queries
   uint64_t bar_kv, bar_full[kStages], bar_empty[kStages];
   uint64_t bar_sdp_full[2], bar_p_ready[2], bar_mma_done[2], bar_dq_full[2], bar_dq_empty[2];
@@ -93,7 +101,7 @@ struct StepIter {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(144)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const BamAttnBwdParams p) {
@@ -370,10 +378,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (a[0] == 0x7fc00001u) red_add(dst, 1.f);   // keep the loads live, skip the reductions
       continue;
 #endif
+#if BAM_DQ_BULK
+      // staging buffer free once the previous bulk reduce has read it
+      const bool dq_leader = threadIdx.x == kWarpDQ * 32;
+      if (dq_leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) sm.dq_stage[i * 128 + d] = __uint_as_float(a[i]);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) sm.dq_stage[(32 + i) * 128 + d] = __uint_as_float(c2[i]);
+      fence_async_smem();
+      named_bar_sync(1, 128);
+      if (dq_leader) {
+        float* gdst = dst - d;   // 64 rows x 512 B contiguous in the head-major accumulator
+        asm volatile(
+            "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n\t"
+            "cp.async.bulk.commit_group;" ::"l"(gdst),
+            "r"(smem_u32(sm.dq_stage)), "n"(64 * 128 * 4)
+            : "memory");
+      }
+#else
       red_add_rows<0>(dst, a);
       red_add_rows<32>(dst, c2);
+#endif
       BAM_TRACE_EV(trace_cta && threadIdx.x == kWarpDQ * 32, 9, s);
     }
+#if BAM_DQ_BULK
+    if (threadIdx.x == kWarpDQ * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
   }
   tc_fence_before();
   __syncthreads();
