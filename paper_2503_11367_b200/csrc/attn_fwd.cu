@@ -281,7 +281,7 @@ struct PairSmem {
   uint32_t tmem_base;
 };
 
-__global__ void __maxnreg__(200)
+__global__ void __maxnreg__(168)
     attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p) {
