@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=2)
+    ap.add_argument("--groups", type=int, default=2,
+                    help="KV-head groups pipelining the CP collectives with compute (N > 1)")
     return ap.parse_args()
 
 
@@ -225,22 +227,24 @@ def main():
     flop_local_fwd = 4.0 * D * Hq * n_allowed / world
     flop_local_bwd = 10.0 * D * Hq * n_allowed / world
 
+    n_groups = args.groups if world > 1 else 1
+
     def step(ev):
+        """ev: [fwd start, fwd end, bwd end, (main start, main end) per head group...]"""
         if world > 1:
-            k_all, v_all = CP.gather_kv(k_loc, v_loc, layout)
-        else:
-            k_all, v_all = k_loc, v_loc
+            ev[0].record()
+            o, lse, gathered = CP.cp_forward(q_loc, k_loc, v_loc, plan, groups=n_groups)
+            ev[1].record()
+            timers = [(ev[3 + 2 * i], ev[4 + 2 * i]) for i in range(len(gathered))]
+            dq, dk, dv = CP.cp_backward(q_loc, gathered, o, lse, do_loc, plan, timers=timers)
+            ev[2].record()
+            return dq, dk, dv
         ev[0].record()
-        o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn)
+        o, lse = A.attn_forward(q_loc, k_loc, v_loc, plan.attn)
         ev[1].record()
-        dq, dk_all, dv_all = A.attn_backward(q_loc, k_all, v_all, o, lse, do_loc, plan.attn,
-                                             dkv_fp32=True, timer=(ev[2], ev[3]))
-        ev[4].record()
-        if world > 1:
-            dk, dv = CP.scatter_dkv(dk_all, dv_all, layout)
-        else:
-            dk, dv = dk_all, dv_all
-        dk, dv = A.to_bf16(dk.contiguous()), A.to_bf16(dv.contiguous())
+        dq, dk, dv = A.attn_backward(q_loc, k_loc, v_loc, o, lse, do_loc, plan.attn,
+                                     timer=(ev[3], ev[4]))
+        ev[2].record()
         return dq, dk, dv
 
     def barrier():
@@ -248,7 +252,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(5)]  # noqa: E731
+    mk = lambda: [torch.cuda.Event(enable_timing=True)  # noqa: E731
+                  for _ in range(3 + 2 * n_groups)]
     for _ in range(args.warmup):
         step(mk())
     barrier()
@@ -265,8 +270,9 @@ def main():
     launches = _lib.launch_count - launches0
     elapsed = start.elapsed_time(end)
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    bwd_main_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
-    bwd_ms = sum(e[1].elapsed_time(e[4]) for e in evs) / args.steps
+    bwd_main_ms = sum(e[3 + 2 * i].elapsed_time(e[4 + 2 * i])
+                      for e in evs for i in range(n_groups)) / args.steps
+    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     compute_ms = fwd_ms + bwd_ms
     t = torch.tensor([elapsed, compute_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -296,7 +302,7 @@ def main():
         kd.requires_grad_(True)
         vd.requires_grad_(True)
         if world > 1:
-            o = CP.cp_bitfield_attention(qd, kd, vd, plan)
+            o = CP.cp_bitfield_attention(qd, kd, vd, plan, groups=n_groups)
         else:
             o = A.bitfield_attention(qd, kd, vd, plan.attn)
         o.backward(dod)
@@ -349,6 +355,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": cfg["name"], "tokens": T, "Hq": Hq, "Hkv": Hkv, "head_dim": D,
                        "cp": world, "policy": args.policy, "n_allowed": n_allowed,
+                       "kv_head_groups": n_groups,
                        "flop_per_step": flop_step,
                        "l2": "inputs larger than L2 (Q alone %.2f GiB per rank)" %
                              (q_loc.numel() * 2 / 2**30)},

@@ -144,6 +144,8 @@ typedef struct BamAttnFwdParams {
   const int32_t* order;     /* [nq] local q-block processing order (heavy first), or NULL */
   int32_t nq, nb, k_rows, Hq, Hkv;
   float scale;              /* softmax scale, usually 1/sqrt(128) */
+  int32_t h_begin, nh;      /* head group: query heads [h_begin, h_begin+nh) of q/o/lse against
+                               the Hkv heads of k/v (nh = 0: all Hq heads) */
 } BamAttnFwdParams;
 int bam_attn_fwd(const BamAttnFwdParams* p, void* stream);
 
@@ -171,6 +173,7 @@ typedef struct BamAttnBwdParams {
   const int32_t* order;     /* [nb] key-block processing order, or NULL */
   int32_t nq, nb, k_rows, Hq, Hkv;
   float scale;
+  int32_t h_begin, nh;      /* head group as in BamAttnFwdParams; k/v/dk/dv hold Hkv heads */
 } BamAttnBwdParams;
 int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
 /* The three launches bam_attn_bwd performs, exposed for per-kernel timing:

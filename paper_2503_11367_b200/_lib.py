@@ -29,7 +29,7 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("desc", c_vp), ("q_gid", c_vp), ("k_row", c_vp), ("row_off", c_vp),
                 ("row_tiles", c_vp), ("order", c_vp),
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
-                ("scale", c_f32)]
+                ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32)]
 
 
 class BamAttnBwdParams(ctypes.Structure):
@@ -38,7 +38,7 @@ class BamAttnBwdParams(ctypes.Structure):
                 ("dv", c_vp), ("desc", c_vp), ("q_gid", c_vp), ("k_row", c_vp),
                 ("col_off", c_vp), ("col_tiles", c_vp), ("order", c_vp),
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
-                ("scale", c_f32)]
+                ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32)]
 
 
 # name -> (restype, argtypes); mirrors include/bam.h exactly

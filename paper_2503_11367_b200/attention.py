@@ -113,20 +113,91 @@ def _check_qkv(q, k, v, plan: AttentionPlan):
         raise ValueError("Hq must be a multiple of Hkv")
 
 
-def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None):
-    """Returns (o bf16 [nq*128, Hq, 128], lse fp32 [Hq, nq*128])."""
-    _check_qkv(q, k, v, plan)
-    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+def _check_group(Hq, Hkv, h_begin, nh):
+    nh = nh or Hq
+    if h_begin < 0 or h_begin + nh > Hq or nh % Hkv:
+        raise ValueError(f"head group [{h_begin}, {h_begin + nh}) of Hq={Hq} over Hkv={Hkv}")
+    return nh
+
+
+def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
+                 h_begin: int = 0, nh: int = 0, out=None):
+    """Returns (o bf16 [nq*128, Hq, 128], lse fp32 [Hq, nq*128]).
+
+    Head groups (context-parallel pipelining): with ``nh`` > 0 only query
+    heads [h_begin, h_begin+nh) are computed, against the ``k.shape[1]`` KV
+    heads of ``k``/``v``; ``out=(o, lse)`` receives them in place."""
     Hq, Hkv = q.shape[1], k.shape[1]
-    o = torch.empty_like(q)
-    lse = torch.empty(Hq, q.shape[0], dtype=torch.float32, device=q.device)
+    if nh or h_begin:
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor")
+    else:
+        _check_qkv(q, k, v, plan)
+    nh = _check_group(Hq, Hkv, h_begin, nh)
+    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+    if out is None:
+        o = torch.empty_like(q)
+        lse = torch.empty(Hq, q.shape[0], dtype=torch.float32, device=q.device)
+    else:
+        o, lse = out
     p = _lib.BamAttnFwdParams(
         q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
         plan.desc.data_ptr(), plan.q_gid.data_ptr(), plan.k_row.data_ptr(),
         plan.row_off.data_ptr(), plan.row_tiles.data_ptr(), plan.fwd_order.data_ptr(),
-        plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale)
+        plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale, h_begin, nh)
     _lib.call("bam_attn_fwd", p)
     return o, lse
+
+
+class BackwardWorkspace:
+    """Per-call backward state: the (lse*log2e, D) pairs and the fp32 dQ
+    accumulator shared by every head group's main kernel."""
+
+    def __init__(self, q, o, lse, do, plan: AttentionPlan, scale):
+        for name, t in (("o", o), ("do", do)):
+            if t.shape != q.shape or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous bf16 tensor shaped like q")
+        self.q, self.o, self.lse, self.do, self.plan = q, o, lse, do, plan
+        self.scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
+        Hq, dev = q.shape[1], q.device
+        self.delta = torch.empty(Hq, q.shape[0], 2, dtype=torch.float32, device=dev)
+        self.dq_acc = torch.empty(Hq, q.shape[0], 128, dtype=torch.float32, device=dev)
+        self.dq = torch.empty_like(q)
+        # preprocess and finalize only touch q-shaped buffers: k/v pointers unused there
+        self._call("bam_attn_bwd_preprocess", q, q, q, q, 0, 0, 1)
+
+    def _params(self, k, v, dk, dv, h_begin, nh, Hkv):
+        pl = self.plan
+        return _lib.BamAttnBwdParams(
+            self.q.data_ptr(), k.data_ptr(), v.data_ptr(), self.o.data_ptr(), self.do.data_ptr(),
+            self.lse.data_ptr(), self.delta.data_ptr(), self.dq_acc.data_ptr(),
+            self.dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), pl.desc.data_ptr(),
+            pl.q_gid.data_ptr(), pl.k_row.data_ptr(), pl.col_off.data_ptr(),
+            pl.col_tiles.data_ptr(), pl.bwd_order.data_ptr(), pl.nq, pl.nb, pl.k_rows,
+            self.q.shape[1], Hkv, self.scale, h_begin, nh)
+
+    def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv):
+        _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv))
+
+    def main(self, k, v, *, h_begin=0, nh=0, timer=None):
+        """dK/dV fp32 partials [k_rows*128, Hkv, 128] of the head group; dQ accumulates."""
+        Hkv = k.shape[1]
+        nh = _check_group(self.q.shape[1], Hkv, h_begin, nh)
+        if k.shape != v.shape or k.shape[0] != self.plan.k_rows * BLOCK or not k.is_contiguous():
+            raise ValueError(f"k/v must be contiguous [{self.plan.k_rows * BLOCK}, Hkv, 128]")
+        dk = torch.empty(k.shape, dtype=torch.float32, device=k.device)
+        dv = torch.empty(k.shape, dtype=torch.float32, device=k.device)
+        if timer is not None:
+            timer[0].record()
+        self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv)
+        if timer is not None:
+            timer[1].record()
+        return dk, dv
+
+    def finalize(self):
+        self._call("bam_attn_bwd_finalize", self.q, self.q, self.q, self.q, 0, 0, 1)
+        return self.dq
 
 
 def attn_backward(q, k, v, o, lse, do, plan: AttentionPlan, scale: float | None = None,
@@ -134,31 +205,9 @@ def attn_backward(q, k, v, o, lse, do, plan: AttentionPlan, scale: float | None 
     """Returns (dq bf16, dk, dv) with dk/dv fp32 [k_rows*128, Hkv, 128]
     partials when ``dkv_fp32`` (for a CP reduce-scatter), else bf16."""
     _check_qkv(q, k, v, plan)
-    for name, t in (("o", o), ("do", do)):
-        if t.shape != q.shape or t.dtype != torch.bfloat16 or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous bf16 tensor shaped like q")
-    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
-    Hq, Hkv = q.shape[1], k.shape[1]
-    dev = q.device
-    delta = torch.empty(Hq, q.shape[0], 2, dtype=torch.float32, device=dev)
-    dq_acc = torch.empty(Hq, q.shape[0], 128, dtype=torch.float32, device=dev)
-    dq = torch.empty_like(q)
-    dk = torch.empty(k.shape, dtype=torch.float32, device=dev)
-    dv = torch.empty(k.shape, dtype=torch.float32, device=dev)
-    p = _lib.BamAttnBwdParams(
-        q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(),
-        delta.data_ptr(), dq_acc.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
-        plan.desc.data_ptr(), plan.q_gid.data_ptr(), plan.k_row.data_ptr(),
-        plan.col_off.data_ptr(), plan.col_tiles.data_ptr(), plan.bwd_order.data_ptr(),
-        plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale)
-    if timer is None:
-        _lib.call("bam_attn_bwd", p)
-    else:   # per-launch CUDA events around the main tcgen05 kernel (bench.py)
-        _lib.call("bam_attn_bwd_preprocess", p)
-        timer[0].record()
-        _lib.call("bam_attn_bwd_main", p)
-        timer[1].record()
-        _lib.call("bam_attn_bwd_finalize", p)
+    ws = BackwardWorkspace(q, o, lse, do, plan, scale)
+    dk, dv = ws.main(k, v, timer=timer)
+    dq = ws.finalize()
     if dkv_fp32:
         return dq, dk, dv
     return dq, to_bf16(dk), to_bf16(dv)

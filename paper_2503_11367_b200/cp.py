@@ -17,7 +17,9 @@ rank's K/V shard is padded to ``max_blocks`` rows for the collectives.
 
 Exchange steps (the only cross-rank traffic): ``gather_kv`` (all-gather of
 K and V) and ``scatter_dkv`` (fp32 reduce-scatter of the dK/dV partials).
-K and V are gathered on a side stream, V overlapping the K-only work.
+Both run per KV-head group on a side stream: the forward of group g starts
+when its K/V land (overlapping the gather of group g+1); the reduce-scatter
+of group g overlaps the backward kernel of group g+1.
 """
 
 from __future__ import annotations
@@ -137,36 +139,106 @@ def make_cp_plan(mask_or_desc, world: int, rank: int, policy: str = "lpt") -> CP
     return CPPlan(layout=layout, attn=attn, assignment=asg, policy=policy)
 
 
-def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None):
-    k_all, v_all = gather_kv(k_loc, v_loc, plan.layout, group)
-    o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn, scale)
-    return o, lse, k_all, v_all
+_COMM_STREAMS: dict = {}
 
 
-def cp_backward(q_loc, k_all, v_all, o, lse, do, plan: CPPlan, group=None, scale=None):
-    dq, dk_all, dv_all = A.attn_backward(q_loc, k_all, v_all, o, lse, do, plan.attn, scale,
-                                         dkv_fp32=True)
-    dk, dv = scatter_dkv(dk_all, dv_all, plan.layout, group)
+def _comm_stream(device) -> torch.cuda.Stream:
+    s = _COMM_STREAMS.get(device)
+    if s is None:
+        s = _COMM_STREAMS[device] = torch.cuda.Stream(device=device)
+    return s
+
+
+def _head_groups(Hkv: int, groups: int):
+    groups = max(1, min(groups, Hkv))
+    while Hkv % groups:
+        groups -= 1
+    per = Hkv // groups
+    return [(g * per, per) for g in range(groups)]
+
+
+def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups: int = 2):
+    """All-gather K/V per KV-head group on a side stream; the forward of group
+    g starts as soon as its K/V have landed, overlapping the gather of group
+    g+1 (the paper overlaps communication per head).
+    Returns (o, lse, [(k_all_g, v_all_g)])."""
+    Hq, Hkv = q_loc.shape[1], k_loc.shape[1]
+    grp = Hq // Hkv
+    cur = torch.cuda.current_stream()
+    comm = _comm_stream(q_loc.device)
+    o = torch.empty_like(q_loc)
+    lse = torch.empty(Hq, q_loc.shape[0], dtype=torch.float32, device=q_loc.device)
+    gathered, events = [], []
+    comm.wait_stream(cur)
+    with torch.cuda.stream(comm):
+        for kv0, nkv in _head_groups(Hkv, groups):
+            kg = k_loc[:, kv0:kv0 + nkv].contiguous()
+            vg = v_loc[:, kv0:kv0 + nkv].contiguous()
+            k_all, v_all = gather_kv(kg, vg, plan.layout, group)
+            ev = torch.cuda.Event()
+            ev.record(comm)
+            gathered.append((k_all, v_all))
+            events.append(ev)
+    for (kv0, nkv), (k_all, v_all), ev in zip(_head_groups(Hkv, groups), gathered, events):
+        cur.wait_event(ev)
+        k_all.record_stream(cur)
+        v_all.record_stream(cur)
+        A.attn_forward(q_loc, k_all, v_all, plan.attn, scale, h_begin=kv0 * grp, nh=nkv * grp,
+                       out=(o, lse))
+    return o, lse, gathered
+
+
+def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=None,
+                timers=None):
+    """Per KV-head group: backward kernel -> fp32 dK/dV partials of every key,
+    reduce-scattered on the side stream while the next group computes."""
+    Hq = q_loc.shape[1]
+    Hkv = sum(k.shape[1] for k, _ in gathered)
+    grp = Hq // Hkv
+    cur = torch.cuda.current_stream()
+    comm = _comm_stream(q_loc.device)
+    ws = A.BackwardWorkspace(q_loc, o, lse, do, plan.attn, scale)
+    parts, kv0 = [], 0
+    for i, (k_all, v_all) in enumerate(gathered):
+        nkv = k_all.shape[1]
+        dk_all, dv_all = ws.main(k_all, v_all, h_begin=kv0 * grp, nh=nkv * grp,
+                                 timer=None if timers is None else timers[i])
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        with torch.cuda.stream(comm):
+            comm.wait_event(ev)
+            dk_all.record_stream(comm)
+            dv_all.record_stream(comm)
+            parts.append(scatter_dkv(dk_all, dv_all, plan.layout, group))
+        kv0 += nkv
+    dq = ws.finalize()
+    cur.wait_stream(comm)
+    dk = torch.cat([p[0] for p in parts], dim=1) if len(parts) > 1 else parts[0][0]
+    dv = torch.cat([p[1] for p in parts], dim=1) if len(parts) > 1 else parts[0][1]
     return dq, A.to_bf16(dk.contiguous()), A.to_bf16(dv.contiguous())
 
 
 class _CPAttention(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, plan, group, scale):
-        o, lse, k_all, v_all = cp_forward(q, k, v, plan, group, scale)
-        ctx.save_for_backward(q, k_all, v_all, o, lse)
+    def forward(ctx, q, k, v, plan, group, scale, groups):
+        o, lse, gathered = cp_forward(q, k, v, plan, group, scale, groups)
+        flat = [t for kv in gathered for t in kv]
+        ctx.save_for_backward(q, o, lse, *flat)
         ctx.plan, ctx.group, ctx.scale = plan, group, scale
         return o
 
     @staticmethod
     def backward(ctx, do):
-        q, k_all, v_all, o, lse = ctx.saved_tensors
-        dq, dk, dv = cp_backward(q, k_all, v_all, o, lse, do.contiguous(), ctx.plan, ctx.group,
+        q, o, lse, *flat = ctx.saved_tensors
+        gathered = list(zip(flat[0::2], flat[1::2]))
+        dq, dk, dv = cp_backward(q, gathered, o, lse, do.contiguous(), ctx.plan, ctx.group,
                                  ctx.scale)
-        return dq, dk, dv, None, None, None
+        return dq, dk, dv, None, None, None, None
 
 
-def cp_bitfield_attention(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None):
+def cp_bitfield_attention(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None,
+                          groups: int = 2):
     """Context-parallel bitfield attention with autograd.  Inputs are this
-    rank's rows (``shard_rows``) of q/k/v; returns this rank's O rows."""
-    return _CPAttention.apply(q_loc, k_loc, v_loc, plan, group, scale)
+    rank's rows (``shard_rows``) of q/k/v; returns this rank's O rows.  K/V
+    travel in ``groups`` KV-head groups so communication overlaps compute."""
+    return _CPAttention.apply(q_loc, k_loc, v_loc, plan, group, scale, groups)

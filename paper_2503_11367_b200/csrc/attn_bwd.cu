@@ -87,8 +87,8 @@ struct StepInfo {
 struct StepIter {
   const int32_t* col;
   int per_j, h0, ci = 0, r = 0;
-  __device__ __forceinline__ StepIter(const int32_t* c, int grp, int hkv)
-      : col(c), per_j(2 * grp), h0(hkv * grp) {}
+  __device__ __forceinline__ StepIter(const int32_t* c, int grp, int hkv, int h_begin)
+      : col(c), per_j(2 * grp), h0(h_begin + hkv * grp) {}
   __device__ __forceinline__ StepInfo get() const {
     const int e = col[ci];
     return {h0 + (r >> 1), e >> 2, e & 3, r & 1};
@@ -110,7 +110,7 @@ __global__ void __maxnreg__(144)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int hkv = blockIdx.x;
   const int kb = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
-  const int grp = p.Hq / p.Hkv;
+  const int grp = (p.nh > 0 ? p.nh : p.Hq) / p.Hkv;
   const int c0 = p.col_off[kb], ncol = p.col_off[kb + 1] - c0;
   const int32_t* col = p.col_tiles + c0;
   const int nsteps = ncol * grp * 2;
@@ -162,7 +162,7 @@ __global__ void __maxnreg__(144)
       tma_load_3d_w(&tm_k, &sm.bar_kv, sm.k + kTileBytes / 2, 64, hkv, krow0, leader);
       tma_load_3d_w(&tm_v, &sm.bar_kv, sm.v, 0, hkv, krow0, leader);
       tma_load_3d_w(&tm_v, &sm.bar_kv, sm.v + kTileBytes / 2, 64, hkv, krow0, leader);
-      StepIter it(col, grp, hkv);
+      StepIter it(col, grp, hkv, p.h_begin);
       for (int s = 0; s < nsteps; ++s) {
         const int st = s % kStages;
         const StepInfo si = it.get();
@@ -270,7 +270,7 @@ __global__ void __maxnreg__(144)
     const long long kg = (long long)kb * 128 + r;
     const long long dk = p.desc[kg];
     const float scale_log2 = p.scale * 1.4426950408889634f;
-    StepIter it(col, grp, hkv);
+    StepIter it(col, grp, hkv, p.h_begin);
     for (int s = 0; s < nsteps; ++s) {
       const int st = s % kStages, b = s & 1;
       const StepInfo si = it.get();
@@ -358,7 +358,7 @@ __global__ void __maxnreg__(144)
     // sit at compile-time 512-B strides from one base (immediate offsets).
     const int d = (warp - kWarpDQ) * 32 + lane;
     const uint32_t lane_base = ((warp - kWarpDQ) * 32) << 16;
-    StepIter it(col, grp, hkv);
+    StepIter it(col, grp, hkv, p.h_begin);
     for (int s = 0; s < nsteps; ++s) {
       const int b = s & 1;
       const StepInfo si = it.get();
@@ -464,8 +464,11 @@ static int check_bwd(const BamAttnBwdParams* pp) {
   const BamAttnBwdParams& p = *pp;
   BAM_CHECK_ARG(p.nq >= 1 && p.nb >= 1 && p.k_rows >= 1, "bam_attn_bwd: nq=%d nb=%d k_rows=%d",
                 p.nq, p.nb, p.k_rows);
-  BAM_CHECK_ARG(p.Hq >= 1 && p.Hkv >= 1 && p.Hq % p.Hkv == 0,
-                "bam_attn_bwd: Hq=%d must be a multiple of Hkv=%d", p.Hq, p.Hkv);
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  BAM_CHECK_ARG(p.Hq >= 1 && p.Hkv >= 1 && nh % p.Hkv == 0 && p.h_begin >= 0 &&
+                    p.h_begin + nh <= p.Hq,
+                "bam_attn_bwd: head group [%d, %d) of Hq=%d over Hkv=%d", p.h_begin,
+                p.h_begin + nh, p.Hq, p.Hkv);
   BAM_CHECK_ARG(p.nb <= 65535, "bam_attn_bwd: nb=%d > 65535", p.nb);
   return kOk;
 }

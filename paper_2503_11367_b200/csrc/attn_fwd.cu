@@ -167,9 +167,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                       ~uintptr_t(1023));
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int h = blockIdx.x;
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  const int h = p.h_begin + blockIdx.x;
   const int j = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
-  const int hkv = h / (p.Hq / p.Hkv);
+  const int hkv = (h - p.h_begin) / (nh / p.Hkv);
   const int t0 = p.row_off[j], n = p.row_off[j + 1] - t0;
   const int32_t* tiles = p.row_tiles + t0;
 
@@ -288,9 +289,10 @@ __global__ void __maxnreg__(168)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int h0 = 2 * blockIdx.x;
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  const int h0 = p.h_begin + 2 * blockIdx.x;
   const int j = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
-  const int hkv = h0 / (p.Hq / p.Hkv);
+  const int hkv = (h0 - p.h_begin) / (nh / p.Hkv);
   const int t0 = p.row_off[j], n = p.row_off[j + 1] - t0;
   const int32_t* tiles = p.row_tiles + t0;
 
@@ -422,27 +424,30 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
   const BamAttnFwdParams& p = *pp;
   BAM_CHECK_ARG(p.nq >= 1 && p.nb >= 1 && p.k_rows >= 1, "bam_attn_fwd: nq=%d nb=%d k_rows=%d",
                 p.nq, p.nb, p.k_rows);
-  BAM_CHECK_ARG(p.Hq >= 1 && p.Hkv >= 1 && p.Hq % p.Hkv == 0,
-                "bam_attn_fwd: Hq=%d must be a multiple of Hkv=%d", p.Hq, p.Hkv);
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  BAM_CHECK_ARG(p.Hq >= 1 && p.Hkv >= 1 && nh % p.Hkv == 0 && p.h_begin >= 0 &&
+                    p.h_begin + nh <= p.Hq,
+                "bam_attn_fwd: head group [%d, %d) of Hq=%d over Hkv=%d", p.h_begin,
+                p.h_begin + nh, p.Hq, p.Hkv);
   BAM_CHECK_ARG(p.nq <= 65535, "bam_attn_fwd: nq=%d > 65535", p.nq);
   CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
-  const int grp = p.Hq / p.Hkv;
+  const int grp = nh / p.Hkv;
   if (grp % 2 == 0) {  // GQA: two query heads share each K/V tile
     const int smem = (int)sizeof(fwd::PairSmem);
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_pair_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid(p.Hq / 2, p.nq);
+    dim3 grid(nh / 2, p.nq);
     fwd::attn_fwd_pair_kernel<<<grid, fwd::kPairThreads, smem, (cudaStream_t)stream>>>(mq, mk,
                                                                                        mv, p);
   } else {
     const int smem = (int)sizeof(fwd::Smem) + 1024;
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid(p.Hq, p.nq);
+    dim3 grid(nh, p.nq);
     fwd::attn_fwd_kernel<<<grid, fwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, p);
   }
   BAM_LAUNCH_CHECK();

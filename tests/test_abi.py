@@ -32,9 +32,9 @@ def test_struct_sizes_match_header():
     from paper_2503_11367_b200 import _lib
 
     assert ctypes.sizeof(_lib.BamBlockSummary) == 40
-    # 11 pointers + 5 int32 + float, 8-byte aligned
-    assert ctypes.sizeof(_lib.BamAttnFwdParams) == 11 * 8 + 6 * 4
-    assert ctypes.sizeof(_lib.BamAttnBwdParams) == 17 * 8 + 6 * 4
+    # pointers + 5 int32 + float + 2 int32 (head group), 8-byte aligned
+    assert ctypes.sizeof(_lib.BamAttnFwdParams) == 11 * 8 + 8 * 4
+    assert ctypes.sizeof(_lib.BamAttnBwdParams) == 17 * 8 + 8 * 4
 
 
 def test_ilp_host_entry_point():
