@@ -101,7 +101,7 @@ struct StepIter {
   }
 };
 
-__global__ void __maxnreg__(144)
+__global__ void __maxnreg__(128)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const BamAttnBwdParams p) {
