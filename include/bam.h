@@ -174,6 +174,13 @@ typedef struct BamAttnBwdParams {
   int32_t nq, nb, k_rows, Hq, Hkv;
   float scale;
   int32_t h_begin, nh;      /* head group as in BamAttnFwdParams; k/v/dk/dv hold Hkv heads */
+  /* Optional CTA-pair mode (thread-block clusters of 2 along the key blocks):
+   * when pair_shared != NULL, order = slot_kb[n_slots] (-1 = padding slot),
+   * col_off / col_tiles are per-slot lists from bam_build_pair_lists (class 0
+   * entries allowed), and pairs with pair_shared[p] != 0 multicast each Q/dO
+   * tile to both CTAs (each loads one half). */
+  const int32_t* pair_shared;
+  int32_t n_slots, pad_;
 } BamAttnBwdParams;
 int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
 /* The three launches bam_attn_bwd performs, exposed for per-kernel timing:
@@ -182,6 +189,15 @@ int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
 int bam_attn_bwd_preprocess(const BamAttnBwdParams* p, void* stream);
 int bam_attn_bwd_main(const BamAttnBwdParams* p, void* stream);
 int bam_attn_bwd_finalize(const BamAttnBwdParams* p, void* stream);
+
+/* CTA-pair step lists for the backward: pairs (order[2p], order[2p+1]) of key
+ * blocks; a pair shares its Q/dO stream when the union of the two CSC columns
+ * is at most 9/8 of the longer one (both slots then walk the union, entries
+ * j << 2 | class, class 0 = skip for that slot).  n_slots = 2 ceil(nb/2).
+ * Pass slot_tiles = NULL to get counts/offsets only. */
+int bam_build_pair_lists(const int32_t* col_off, const int32_t* col_tiles, const int32_t* order,
+                         int32_t nb, int32_t* slot_kb, int32_t* slot_cnt, int32_t* slot_off,
+                         int32_t* slot_tiles, int32_t* pair_shared, void* stream);
 
 /* fp32 -> bf16 conversion (dk/dv partials to the bf16 gradient layout). */
 int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);

@@ -38,7 +38,8 @@ class BamAttnBwdParams(ctypes.Structure):
                 ("dv", c_vp), ("desc", c_vp), ("q_gid", c_vp), ("k_row", c_vp),
                 ("col_off", c_vp), ("col_tiles", c_vp), ("order", c_vp),
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
-                ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32)]
+                ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
+                ("pair_shared", c_vp), ("n_slots", c_i32), ("pad_", c_i32)]
 
 
 # name -> (restype, argtypes); mirrors include/bam.h exactly
@@ -65,6 +66,7 @@ SIGNATURES = {
     "bam_attn_bwd_main": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_attn_bwd_finalize": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
+    "bam_build_pair_lists": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bam_selftest_umma": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bam_set_trace_buffer": (c_i32, [c_vp]),
 }
@@ -126,6 +128,7 @@ KERNELS_PER_CALL = {
     "bam_contiguous_assign": 1, "bam_split_count": 2, "bam_split_fill": 1,
     "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
     "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
+    "bam_build_pair_lists": 2,
 }
 launch_count = 0
 

@@ -19,6 +19,7 @@ mask on the device and reused by forward and backward.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -45,6 +46,11 @@ class AttentionPlan:
     col_tiles: torch.Tensor   # int32 j << 2 | class
     fwd_order: torch.Tensor   # int32 [nq] heavy-first local query blocks
     bwd_order: torch.Tensor   # int32 [nb] heavy-first key blocks
+    # backward CTA pairs (clusters of 2 sharing the Q/dO stream), bam_build_pair_lists
+    slot_kb: torch.Tensor | None = None
+    slot_off: torch.Tensor | None = None
+    slot_tiles: torch.Tensor | None = None
+    pair_shared: torch.Tensor | None = None
 
     @property
     def nq(self) -> int:
@@ -89,10 +95,24 @@ def build_plan(desc: torch.Tensor, q_gid: torch.Tensor | None = None,
     _lib.call("bam_build_tile_lists", classes.data_ptr(), nb, q_gid.data_ptr(), nq,
               row_cnt.data_ptr(), row_off.data_ptr(), row_tiles.data_ptr(), col_cnt.data_ptr(),
               col_off.data_ptr(), col_tiles.data_ptr())
+    bwd_order = _heavy_first(col_cnt)
+    npairs = (nb + 1) // 2
+    slot_kb = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
+    slot_cnt = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
+    slot_off = torch.empty(2 * npairs + 1, dtype=torch.int32, device=dev)
+    pair_shared = torch.empty(npairs, dtype=torch.int32, device=dev)
+    _lib.call("bam_build_pair_lists", col_off.data_ptr(), col_tiles.data_ptr(),
+              bwd_order.data_ptr(), nb, slot_kb.data_ptr(), slot_cnt.data_ptr(),
+              slot_off.data_ptr(), None, pair_shared.data_ptr())
+    slot_tiles = torch.empty(max(int(slot_off[-1].item()), 1), dtype=torch.int32, device=dev)
+    _lib.call("bam_build_pair_lists", col_off.data_ptr(), col_tiles.data_ptr(),
+              bwd_order.data_ptr(), nb, slot_kb.data_ptr(), slot_cnt.data_ptr(),
+              slot_off.data_ptr(), slot_tiles.data_ptr(), pair_shared.data_ptr())
     return AttentionPlan(desc=desc, nb=nb, classes=classes, W=W, q_gid=q_gid.to(torch.int32),
                          k_row=k_row.to(torch.int32), k_rows=int(k_rows), row_off=row_off,
                          row_tiles=row_tiles, col_off=col_off, col_tiles=col_tiles,
-                         fwd_order=_heavy_first(row_cnt), bwd_order=_heavy_first(col_cnt))
+                         fwd_order=_heavy_first(row_cnt), bwd_order=bwd_order, slot_kb=slot_kb,
+                         slot_off=slot_off, slot_tiles=slot_tiles, pair_shared=pair_shared)
 
 
 def plan_for_mask(mask: BitfieldMask) -> AttentionPlan:
@@ -169,13 +189,18 @@ class BackwardWorkspace:
 
     def _params(self, k, v, dk, dv, h_begin, nh, Hkv):
         pl = self.plan
+        pairs = pl.pair_shared is not None and os.environ.get("BAM_BWD_PAIRS", "1") != "0"
+        col_off, col_tiles, order = ((pl.slot_off, pl.slot_tiles, pl.slot_kb) if pairs else
+                                     (pl.col_off, pl.col_tiles, pl.bwd_order))
         return _lib.BamAttnBwdParams(
             self.q.data_ptr(), k.data_ptr(), v.data_ptr(), self.o.data_ptr(), self.do.data_ptr(),
             self.lse.data_ptr(), self.delta.data_ptr(), self.dq_acc.data_ptr(),
             self.dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), pl.desc.data_ptr(),
-            pl.q_gid.data_ptr(), pl.k_row.data_ptr(), pl.col_off.data_ptr(),
-            pl.col_tiles.data_ptr(), pl.bwd_order.data_ptr(), pl.nq, pl.nb, pl.k_rows,
-            self.q.shape[1], Hkv, self.scale, h_begin, nh)
+            pl.q_gid.data_ptr(), pl.k_row.data_ptr(), col_off.data_ptr(),
+            col_tiles.data_ptr(), order.data_ptr(), pl.nq, pl.nb, pl.k_rows,
+            self.q.shape[1], Hkv, self.scale, h_begin, nh,
+            pl.pair_shared.data_ptr() if pairs else None,
+            int(pl.slot_kb.shape[0]) if pairs else 0, 0)
 
     def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv):
         _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv))

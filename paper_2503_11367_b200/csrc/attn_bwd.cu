@@ -25,6 +25,7 @@
 //   MMA issuer + TMEM alloc, warp 13 TMA producer (Q/dO half tiles + LSE/D).
 #include "../../include/bam.h"
 #include "common.cuh"
+#include "scan.cuh"
 #include "tma.h"
 
 namespace bam {
@@ -109,13 +110,24 @@ __global__ void __maxnreg__(128)
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int hkv = blockIdx.x;
-  const int kb = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
+  // CTA-pair mode: clusters of 2 along y; slot lists; shared pairs multicast Q/dO
+  const bool cluster_mode = p.pair_shared != nullptr;
+  const int slot = blockIdx.y;
+  const int kb = p.order ? p.order[slot] : slot;   // -1: padding slot (cluster mode)
+  const int li = cluster_mode ? slot : kb;         // step-list index
+  const uint32_t crank = cluster_mode ? cluster_ctarank() : 0;
+  const bool shared = cluster_mode && p.pair_shared[slot >> 1] != 0;
   const int grp = (p.nh > 0 ? p.nh : p.Hq) / p.Hkv;
-  const int c0 = p.col_off[kb], ncol = p.col_off[kb + 1] - c0;
-  const int32_t* col = p.col_tiles + c0;
+  int ncol = 0, krow0 = 0;
+  const int32_t* col = p.col_tiles;
+  if (kb >= 0) {
+    const int c0 = p.col_off[li];
+    ncol = p.col_off[li + 1] - c0;
+    col = p.col_tiles + c0;
+    krow0 = p.k_row[kb] * 128;
+  }
   const int nsteps = ncol * grp * 2;
   const int64_t Tq = (int64_t)p.nq * 128;
-  const int krow0 = p.k_row[kb] * 128;
   const bool trace_cta = blockIdx.x == 0 && blockIdx.y == 0;
   (void)trace_cta;
 #ifdef BAM_TRACE
@@ -127,7 +139,7 @@ __global__ void __maxnreg__(128)
     mbar_init(&sm.bar_kv, 1);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&sm.bar_full[i], 1);
-      mbar_init(&sm.bar_empty[i], 1);
+      mbar_init(&sm.bar_empty[i], shared ? 2 : 1);  // shared: both CTAs' MMAs release a stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.bar_sdp_full[b], 1);
@@ -144,6 +156,7 @@ __global__ void __maxnreg__(128)
   }
   tc_fence_before();
   __syncthreads();
+  if (cluster_mode) cluster_sync_all();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
@@ -172,10 +185,19 @@ __global__ void __maxnreg__(128)
         BAM_TRACE_EV(trace_cta && leader, 10, s);
         Stage& S = sm.st[st];
         mbar_expect_tx_w(&sm.bar_full[st], 2 * kHalfBytes + 512, leader);
-        tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0, leader);
-        tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q + kHalfBytes / 2, 64, si.h, row0, leader);
-        tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout, 0, si.h, row0, leader);
-        tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0, leader);
+        if (shared) {  // this CTA loads column box `crank` of Q and dO for both CTAs
+          const uint32_t off = crank * (kHalfBytes / 2);
+          tma_load_3d_mc_w(&tm_q, &sm.bar_full[st], S.q + off, crank * 64, si.h, row0, 0x3,
+                           leader);
+          tma_load_3d_mc_w(&tm_do, &sm.bar_full[st], S.dout + off, crank * 64, si.h, row0, 0x3,
+                           leader);
+        } else {
+          tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q, 0, si.h, row0, leader);
+          tma_load_3d_w(&tm_q, &sm.bar_full[st], S.q + kHalfBytes / 2, 64, si.h, row0, leader);
+          tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout, 0, si.h, row0, leader);
+          tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0,
+                        leader);
+        }
         bulk_load_w(sm.ld[st], p.delta + 2 * ((int64_t)si.h * Tq + row0), 512, &sm.bar_full[st],
                     leader);
       }
@@ -255,7 +277,10 @@ __global__ void __maxnreg__(128)
         for (int kk = 0; kk < 8; ++kk)
           mma_ss_w(tDQ, dk_kmn + kk * 128, dds + kk * 128, id_q, kk > 0, leader);
         tc_commit_w(&sm.bar_dq_full[b], leader);
-        tc_commit_w(&sm.bar_empty[st], leader);
+        if (shared)
+          tc_commit_mc_w(&sm.bar_empty[st], 0x3, leader);  // the stage is filled by both CTAs
+        else
+          tc_commit_w(&sm.bar_empty[st], leader);
         tc_commit_w(&sm.bar_mma_done[b], leader);
         BAM_TRACE_EV(trace_cta && leader, 3, s);
       }
@@ -284,7 +309,7 @@ __global__ void __maxnreg__(128)
       uint32_t sr[32], dr[32];
       BAM_TMEM_LD32(tS + c * 32, sr);
       BAM_TMEM_LD32(tdP + c * 32, dr);
-      uint32_t allow = 0xFFFFFFFFu;
+      uint32_t allow = si.cls ? 0xFFFFFFFFu : 0u;  // class 0: a pair step this key block skips
       if (si.cls == 2) {  // PARTIAL tile: descriptor predicate for these 32 queries
         const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64 + c * 32;
         allow = 0;
@@ -329,6 +354,8 @@ __global__ void __maxnreg__(128)
       mbar_arrive(&sm.bar_p_ready[b]);
     }
     // epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled), fp32 rows
+    if (kb < 0) goto done;  // padding slot of the last cluster
+    {
     const int64_t row = (int64_t)krow0 + r;
     float* dst = (c == 0 ? p.dv : p.dk) + (row * p.Hkv + hkv) * 128;
     const float mul = c == 0 ? 1.f : p.scale;
@@ -351,6 +378,8 @@ __global__ void __maxnreg__(128)
       float4* d4 = reinterpret_cast<float4*>(dst);
       for (int i = 0; i < 32; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    }
+  done:;
   } else {
     // ------------------------------------------------------------ dQ epilogue warps 8-11
     // TMEM lane = head-dim column d; columns = the 64 queries of the step.  The
@@ -378,6 +407,7 @@ __global__ void __maxnreg__(128)
       if (a[0] == 0x7fc00001u) red_add(dst, 1.f);   // keep the loads live, skip the reductions
       continue;
 #endif
+      if (si.cls == 0) continue;  // pair step this key block skips: dQ^T is zero
 #if BAM_DQ_BULK
       // staging buffer free once the previous bulk reduce has read it
       const bool dq_leader = threadIdx.x == kWarpDQ * 32;
@@ -409,6 +439,7 @@ __global__ void __maxnreg__(128)
   }
   tc_fence_before();
   __syncthreads();
+  if (cluster_mode) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == kWarpMMA) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -451,6 +482,58 @@ __global__ void bwd_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat
     const float4 v = reinterpret_cast<const float4*>(acc + (h * rows + row) * 128)[lane_id()];
     reinterpret_cast<uint2*>(dq + w * 128)[lane_id()] =
         make_uint2(pack_bf16(v.x * scale, v.y * scale), pack_bf16(v.z * scale, v.w * scale));
+  }
+}
+
+// CTA-pair step lists (bam_build_pair_lists): one thread per pair merges the
+// two ascending CSC columns.  Pass 1 (tiles == nullptr) counts, pass 2 fills.
+__global__ void pair_lists_kernel(const int32_t* __restrict__ col_off,
+                                  const int32_t* __restrict__ col_tiles,
+                                  const int32_t* __restrict__ order, int32_t nb,
+                                  int32_t* __restrict__ slot_kb, int32_t* __restrict__ slot_cnt,
+                                  const int32_t* __restrict__ slot_off, int32_t* __restrict__ tiles,
+                                  int32_t* __restrict__ pair_shared) {
+  const int npairs = (nb + 1) / 2;
+  for (int pr = blockIdx.x * blockDim.x + threadIdx.x; pr < npairs; pr += gridDim.x * blockDim.x) {
+    const int a = order[2 * pr], b = 2 * pr + 1 < nb ? order[2 * pr + 1] : -1;
+    const int32_t* ca = col_tiles + col_off[a];
+    const int na = col_off[a + 1] - col_off[a];
+    const int32_t* cb = b >= 0 ? col_tiles + col_off[b] : nullptr;
+    const int nbb = b >= 0 ? col_off[b + 1] - col_off[b] : 0;
+    if (tiles == nullptr) {
+      slot_kb[2 * pr] = a;
+      slot_kb[2 * pr + 1] = b;
+      int u = 0, i = 0, k = 0;
+      while (i < na || k < nbb) {
+        const int ja = i < na ? ca[i] >> 2 : 0x7fffffff, jb = k < nbb ? cb[k] >> 2 : 0x7fffffff;
+        i += ja <= jb;
+        k += jb <= ja;
+        ++u;
+      }
+      const int mx = na > nbb ? na : nbb;
+      const bool sh = b >= 0 && mx > 0 && 8 * u <= 9 * mx;
+      pair_shared[pr] = sh;
+      slot_cnt[2 * pr] = sh ? u : na;
+      slot_cnt[2 * pr + 1] = sh ? u : nbb;
+    } else {
+      int32_t* oa = tiles + slot_off[2 * pr];
+      int32_t* ob = tiles + slot_off[2 * pr + 1];
+      if (pair_shared[pr]) {  // union walk: both slots get every j, class 0 where absent
+        int i = 0, k = 0, n = 0;
+        while (i < na || k < nbb) {
+          const int ja = i < na ? ca[i] >> 2 : 0x7fffffff, jb = k < nbb ? cb[k] >> 2 : 0x7fffffff;
+          const int j = ja < jb ? ja : jb;
+          oa[n] = (j << 2) | (ja == j ? (ca[i] & 3) : 0);
+          ob[n] = (j << 2) | (jb == j ? (cb[k] & 3) : 0);
+          i += ja == j;
+          k += jb == j;
+          ++n;
+        }
+      } else {
+        for (int i = 0; i < na; ++i) oa[i] = ca[i];
+        for (int k = 0; k < nbb; ++k) ob[k] = cb[k];
+      }
+    }
   }
 }
 
@@ -514,8 +597,26 @@ int bam_attn_bwd_main(const BamAttnBwdParams* pp, void* stream) {
   const int smem = (int)sizeof(bwd::Smem);
   BAM_CUDA_TRY(cudaFuncSetAttribute(bwd::attn_bwd_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid(p.Hkv, p.nb);
-  bwd::attn_bwd_kernel<<<grid, bwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, mdo, p);
+  if (p.pair_shared) {  // CTA pairs: clusters of 2 along the (slot) y dimension
+    BAM_CHECK_ARG(p.n_slots >= 2 && p.n_slots % 2 == 0 && p.order != nullptr,
+                  "bam_attn_bwd: pair mode needs an even n_slots=%d and slot_kb", p.n_slots);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.Hkv, p.n_slots);
+    cfg.blockDim = dim3(bwd::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 2;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BAM_CUDA_TRY(cudaLaunchKernelEx(&cfg, bwd::attn_bwd_kernel, mq, mk, mv, mdo, p));
+  } else {
+    dim3 grid(p.Hkv, p.nb);
+    bwd::attn_bwd_kernel<<<grid, bwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, mdo, p);
+  }
   BAM_LAUNCH_CHECK();
   return kOk;
 }
@@ -525,6 +626,26 @@ int bam_attn_bwd_finalize(const BamAttnBwdParams* pp, void* stream) {
   const BamAttnBwdParams& p = *pp;
   bwd::bwd_dq_convert_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
       p.dq_acc, reinterpret_cast<__nv_bfloat16*>(p.dq), (int64_t)p.nq * 128, p.Hq, p.scale);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+int bam_build_pair_lists(const int32_t* col_off, const int32_t* col_tiles, const int32_t* order,
+                         int32_t nb, int32_t* slot_kb, int32_t* slot_cnt, int32_t* slot_off,
+                         int32_t* slot_tiles, int32_t* pair_shared, void* stream) {
+  BAM_CHECK_ARG(nb >= 1 && order != nullptr, "bam_build_pair_lists: nb=%d", nb);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int npairs = (nb + 1) / 2;
+  const int grid = (npairs + 127) / 128;
+  if (slot_tiles == nullptr) {
+    bwd::pair_lists_kernel<<<grid, 128, 0, s>>>(col_off, col_tiles, order, nb, slot_kb, slot_cnt,
+                                                nullptr, nullptr, pair_shared);
+    BAM_LAUNCH_CHECK();
+    scan_kernel<<<1, 1024, 0, s>>>(slot_cnt, 2 * npairs, slot_off);
+  } else {
+    bwd::pair_lists_kernel<<<grid, 128, 0, s>>>(col_off, col_tiles, order, nb, slot_kb, slot_cnt,
+                                                slot_off, slot_tiles, pair_shared);
+  }
   BAM_LAUNCH_CHECK();
   return kOk;
 }

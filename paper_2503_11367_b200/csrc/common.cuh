@@ -264,6 +264,37 @@ __device__ __forceinline__ void bulk_load_w(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "r"(leader)
       : "memory");
 }
+// Multicast variant: the same box lands at the same smem offset in every CTA
+// of `cta_mask` and completes each CTA's mbarrier at the same offset.
+__device__ __forceinline__ void tma_load_3d_mc_w(const CUtensorMap* m, uint64_t* bar, void* dst,
+                                                 int c0, int c1, int c2, uint16_t cta_mask,
+                                                 uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %7, 0;\n\t"
+      "@q cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;\n\t}\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "h"(cta_mask), "r"(leader)
+      : "memory");
+}
+// tcgen05.commit arriving on the mbarrier at `bar`'s offset in every CTA of cta_mask
+__device__ __forceinline__ void tc_commit_mc_w(uint64_t* bar, uint16_t cta_mask, uint32_t leader) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}\n" ::"r"(smem_u32(bar)),
+      "h"(cta_mask), "r"(leader)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx_w(uint64_t* bar, uint32_t bytes, uint32_t leader) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
