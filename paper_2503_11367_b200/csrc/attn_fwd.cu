@@ -42,6 +42,27 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* m, uint64_t* bar, u
   tma_load_3d(m, bar, dst + kTileBytes / 2, 64, head, row0);
 }
 
+#ifndef BAM_FWD_POLY_EVERY
+#define BAM_FWD_POLY_EVERY 2
+#endif
+constexpr int kPolyEvery = BAM_FWD_POLY_EVERY;
+
+// 2^x on the FMA pipe: x = n + f, f in [-0.5, 0.5] (round via the 1.5*2^23
+// magic constant), 2^f by a degree-4 polynomial (rel. err < 4e-6, well below
+// bf16 P rounding), exponent n added to the float bits.  x <= 8 here (lazy
+// rescale); clamping at -127 makes 2^x flush to ~0 like ex2.approx.ftz.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;                 // integer part in the low mantissa bits
+  const float f = x - (t - 12582912.f);           // [-0.5, 0.5]
+  float p = fmaf(1.3333558e-3f, f, 9.6181291e-3f);
+  p = fmaf(p, f, 5.5504109e-2f);
+  p = fmaf(p, f, 2.4022651e-1f);
+  p = fmaf(p, f, 6.9314718e-1f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // Softmax / epilogue role of one 128-row query tile: thread (warp w, lane)
 // owns row r = 32 w + lane = TMEM lane r.  Per key tile t: wait S(t), mask
 // PARTIAL tiles, online softmax (log2 domain, lazy 2^8 rescale of O in TMEM),
@@ -104,8 +125,13 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float p0 = ex2(fmaf(s[c * 32 + 2 * i], scale_log2, -mb));
-        const float p1 = ex2(fmaf(s[c * 32 + 2 * i + 1], scale_log2, -mb));
+        const float x0 = fmaf(s[c * 32 + 2 * i], scale_log2, -mb);
+        const float x1 = fmaf(s[c * 32 + 2 * i + 1], scale_log2, -mb);
+        // a share of the exponentials runs on the FMA pipe so MUFU is not the
+        // softmax bottleneck (every kPolyEvery-th pair's second element)
+        const float p0 = ex2(x0);
+        const float p1 = (kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) ? ex2_poly(x1)
+                                                                                 : ex2(x1);
         l += p0 + p1;
         pk[i] = pack_bf16(p0, p1);
       }
