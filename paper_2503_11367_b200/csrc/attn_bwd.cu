@@ -8,10 +8,11 @@
 // (j outer, head, half inner, so CTAs running together hit the same dQ
 // accumulator lines in L2):
 //   S^T  = K Q^T      (SS, M=128 keys, N=64)  -> TMEM S_b      P^T = exp2(S^T c - LSE)
-//                     (P^T bf16 of queries [32c, 32c+32) over S_b cols [32c, 32c+16))
+//                     (P^T bf16 of queries [32c, 32c+32) over S_b cols [32c, 32c+16),
+//                      dS^T bf16 over [32c+16, 32c+32))
 //   dP^T = V dO^T     (SS)                    -> TMEM dP_b     dS^T = P^T (dP^T - D)
 //   dV  += P^T dO     (TS: P^T bf16 in S_b, dO MN-major)       -> TMEM [0,128)
-//   dK  += dS^T Q     (SS: dS^T smem K-major, Q MN-major)      -> TMEM [128,256)
+//   dK  += dS^T Q     (TS: dS^T bf16 in TMEM S_b, Q MN-major)  -> TMEM [128,256)
 //   dQ^T = K^T dS^T   (SS: K MN-major, dS^T MN-major)          -> TMEM dP_b
 // S_b / dP_b are double-buffered (b = step & 1), so the MMAs of step s+1's
 // S/dP run while the compute warps turn step s into P / dS, and dV/dK/dQ of
@@ -266,10 +267,11 @@ __global__ void __maxnreg__(128)
           mma_ts_w(tmem + kColDV, tS + (kk >> 1) * 32 + (kk & 1) * 8, ddomn + kk * 128, id_kv,
                    (s > 0 || kk > 0), leader);
         BAM_TRACE_EV(trace_cta && leader, 14, s);
-        // dK += dS^T Q   (dS^T K-major: 32 B per 16 queries)
+        // dK += dS^T Q   (A = dS^T from TMEM, like P^T but 16 columns further)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ss_w(tmem + kColDK, dds + kk * 2, dqmn + kk * 128, id_kv, (s > 0 || kk > 0), leader);
+          mma_ts_w(tmem + kColDK, tS + (kk >> 1) * 32 + 16 + (kk & 1) * 8, dqmn + kk * 128, id_kv,
+                   (s > 0 || kk > 0), leader);
         BAM_TRACE_EV(trace_cta && leader, 15, s);
         // dQ^T = K^T dS^T  (K = 128 keys: 8 steps of 16 key rows = 2048 B); dS^T as MN-major
         // B uses the same start address with LBO unused (N = 64 = one swizzle atom)
@@ -336,6 +338,9 @@ __global__ void __maxnreg__(128)
       // P^T (bf16 pairs) goes over the S columns this warpgroup itself read,
       // [32c, 32c+16): the other warpgroup may still be loading its own columns.
       BAM_TMEM_ST16(tS + c * 32, pk);
+      // dS^T (bf16) too: over [32c+16, 32c+32) as the TMEM A operand of dK, and
+      // into shared memory as the B operand of dQ^T
+      BAM_TMEM_ST16(tS + c * 32 + 16, dsk);
       // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
