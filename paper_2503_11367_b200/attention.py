@@ -260,10 +260,41 @@ class _BitfieldAttention(torch.autograd.Function):
         return dq, dk, dv, None, None
 
 
+PAD_BIT = 1 << 60   # descriptor of padding tokens (a modality bit no real token uses)
+
+
+def padded_descriptors(desc: torch.Tensor) -> torch.Tensor:
+    """Pad a descriptor array to a multiple of 128 tokens with PAD_BIT tokens.
+
+    A pure-modality pad token attends only other pad tokens (mask.py:110-112)
+    and no real token attends it: text needs a shared bit (text descriptors
+    carry registered modality bits only) and modality tokens need equality.
+    Needs bit 60 to be unused, i.e. at most 59 registered modalities."""
+    T = desc.shape[0]
+    pad = (-T) % BLOCK
+    if pad == 0:
+        return desc
+    if bool(((desc & PAD_BIT) != 0).any()):
+        raise ValueError("cannot pad a mask that uses modality bit 60 (60 modalities)")
+    return torch.cat([desc, torch.full((pad,), PAD_BIT, dtype=desc.dtype, device=desc.device)])
+
+
 def bitfield_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                        mask_or_plan, scale: float | None = None) -> torch.Tensor:
     """Single-GPU bitfield-masked attention with autograd.
 
-    ``mask_or_plan``: a ``BitfieldMask`` (planned here) or an ``AttentionPlan``."""
-    plan = mask_or_plan if isinstance(mask_or_plan, AttentionPlan) else plan_for_mask(mask_or_plan)
-    return _BitfieldAttention.apply(q, k, v, plan, scale)
+    ``mask_or_plan``: a ``BitfieldMask`` (planned here) or an ``AttentionPlan``.
+    Sequences that are not a multiple of 128 tokens are padded with tokens
+    that nothing attends (``padded_descriptors``); the padding is sliced off."""
+    if isinstance(mask_or_plan, AttentionPlan):
+        return _BitfieldAttention.apply(q, k, v, mask_or_plan, scale)
+    T = q.shape[0]
+    pad = (-T) % BLOCK
+    if pad == 0:
+        return _BitfieldAttention.apply(q, k, v, plan_for_mask(mask_or_plan), scale)
+    plan = build_plan(padded_descriptors(mask_or_plan.device_descriptors()))
+    zq = q.new_zeros((pad,) + tuple(q.shape[1:]))
+    zk = k.new_zeros((pad,) + tuple(k.shape[1:]))
+    o = _BitfieldAttention.apply(torch.cat([q, zq]), torch.cat([k, zk]), torch.cat([v, zk]),
+                                 plan, scale)
+    return o[:T]
