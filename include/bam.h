@@ -146,8 +146,26 @@ typedef struct BamAttnFwdParams {
   float scale;              /* softmax scale, usually 1/sqrt(128) */
   int32_t h_begin, nh;      /* head group: query heads [h_begin, h_begin+nh) of q/o/lse against
                                the Hkv heads of k/v (nh = 0: all Hq heads) */
+  /* Optional intra-GPU split-KV schedule (the paper's subblocks, PAPER.md:564-584;
+   * ref balance.py:223-265): items[n_items] = {query block j, first tile, end
+   * tile, slot}, in LPT order.  slot < 0: the item is the whole row and writes
+   * o/lse; slot >= 0: a subblock writing unnormalised fp32 partials
+   * part_o[slot][Hq][128][128] and (m log2, l) pairs part_ml[slot][Hq][128][2],
+   * merged by bam_attn_fwd_combine.  items == NULL: one whole row per CTA. */
+  const int32_t* items;     /* int4 records */
+  float* part_o;
+  float* part_ml;
+  int32_t n_items;
+  int32_t pad_;
 } BamAttnFwdParams;
 int bam_attn_fwd(const BamAttnFwdParams* p, void* stream);
+
+/* The aggregation kernel of the split schedule: for each combine record
+ * {query block j, first slot, n slots, 0} (combine[n_combine]) and each query
+ * head of the group, O = sum_p 2^(m_p - M) O_p / sum_p 2^(m_p - M) l_p and
+ * LSE = (M + log2 L) ln 2, written to o / lse of p. */
+int bam_attn_fwd_combine(const BamAttnFwdParams* p, const int32_t* combine, int32_t n_combine,
+                         void* stream);
 
 /* Backward.  dq (bf16) for the local rows; dk/dv fp32 partial gradients for
  * every key row of k/v (the contributions of the local queries; summed over

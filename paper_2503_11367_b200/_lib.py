@@ -29,7 +29,9 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("desc", c_vp), ("q_gid", c_vp), ("k_row", c_vp), ("row_off", c_vp),
                 ("row_tiles", c_vp), ("order", c_vp),
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
-                ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32)]
+                ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
+                ("items", c_vp), ("part_o", c_vp), ("part_ml", c_vp), ("n_items", c_i32),
+                ("pad_", c_i32)]
 
 
 class BamAttnBwdParams(ctypes.Structure):
@@ -61,6 +63,7 @@ SIGNATURES = {
     "bam_split_fill": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bam_ilp_optimal": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "bam_attn_fwd": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp]),
+    "bam_attn_fwd_combine": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp, c_i32, c_vp]),
     "bam_attn_bwd": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_attn_bwd_preprocess": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_attn_bwd_main": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
@@ -128,7 +131,7 @@ KERNELS_PER_CALL = {
     "bam_contiguous_assign": 1, "bam_split_count": 2, "bam_split_fill": 1,
     "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
     "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
-    "bam_build_pair_lists": 2,
+    "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1,
 }
 launch_count = 0
 

@@ -140,8 +140,59 @@ def _check_group(Hq, Hkv, h_begin, nh):
     return nh
 
 
+@dataclass
+class SplitSchedule:
+    """Intra-GPU split-KV schedule (the paper's subblocks, PAPER.md:564-584;
+    ref balance.py:217-265): every local query-block row is cut into pieces of
+    at most ``subblock`` key tiles (``split_block``), the pieces are ordered
+    longest first (LPT) and the GPU's block scheduler hands them to SMs as
+    they free up; rows cut into >= 2 pieces are merged by the aggregation
+    kernel (``bam_attn_fwd_combine``)."""
+    subblock: int
+    items: torch.Tensor       # int32 [n_items, 4]: (j, first tile, end tile, slot | -1)
+    combine: torch.Tensor     # int32 [n_combine, 4]: (j, first slot, n pieces, 0)
+    n_slots: int
+
+    @property
+    def n_items(self) -> int:
+        return int(self.items.shape[0])
+
+
+def build_split_schedule(plan: AttentionPlan, subblock: int) -> SplitSchedule:
+    """All on the device: bam_split_count/fill cut the rows, bam_lpt_assign
+    (one unit) orders the pieces by (-size, block, index)."""
+    from .balance import lpt_device
+
+    if subblock < 1:
+        raise ValueError("subblock_size must be >= 1")
+    dev = plan.row_off.device
+    nq = plan.nq
+    cnt = (plan.row_off[1:] - plan.row_off[:-1]).to(torch.int32).contiguous()
+    pcnt = torch.empty(nq, dtype=torch.int32, device=dev)
+    poff = torch.empty(nq + 1, dtype=torch.int32, device=dev)
+    _lib.call("bam_split_count", cnt.data_ptr(), nq, subblock, pcnt.data_ptr(), poff.data_ptr())
+    n_pieces = int(poff[-1].item())
+    size = torch.empty(max(n_pieces, 1), dtype=torch.int32, device=dev)
+    blk, idx = torch.empty_like(size), torch.empty_like(size)
+    _lib.call("bam_split_fill", cnt.data_ptr(), nq, subblock, poff.data_ptr(), size.data_ptr(),
+              blk.data_ptr(), idx.data_ptr())
+    size, blk, idx = size[:n_pieces], blk[:n_pieces], idx[:n_pieces]
+    split = pcnt[blk.long()] >= 2
+    slot = torch.where(split, torch.cumsum(split.to(torch.int32), 0) - 1,
+                       torch.full_like(size, -1)).to(torch.int32)
+    t0 = idx * subblock
+    rec = torch.stack([blk, t0, t0 + size, slot], dim=1).to(torch.int32)
+    order = lpt_device(size.contiguous(), 1).flat.long()      # LPT: (-size, block, index)
+    items = rec[order].contiguous()
+    first = split & (idx == 0)
+    comb = torch.stack([blk[first], slot[first], pcnt[blk[first].long()],
+                        torch.zeros_like(blk[first])], dim=1).to(torch.int32).contiguous()
+    return SplitSchedule(subblock=subblock, items=items, combine=comb,
+                         n_slots=int(split.sum().item()))
+
+
 def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
-                 h_begin: int = 0, nh: int = 0, out=None):
+                 h_begin: int = 0, nh: int = 0, out=None, schedule: SplitSchedule | None = None):
     """Returns (o bf16 [nq*128, Hq, 128], lse fp32 [Hq, nq*128]).
 
     Head groups (context-parallel pipelining): with ``nh`` > 0 only query
@@ -161,12 +212,23 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         lse = torch.empty(Hq, q.shape[0], dtype=torch.float32, device=q.device)
     else:
         o, lse = out
+    part_o = part_ml = None
+    if schedule is not None and schedule.n_slots:
+        part_o = torch.empty(schedule.n_slots, Hq, 128, 128, dtype=torch.float32, device=q.device)
+        part_ml = torch.empty(schedule.n_slots, Hq, 128, 2, dtype=torch.float32, device=q.device)
     p = _lib.BamAttnFwdParams(
         q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
         plan.desc.data_ptr(), plan.q_gid.data_ptr(), plan.k_row.data_ptr(),
         plan.row_off.data_ptr(), plan.row_tiles.data_ptr(), plan.fwd_order.data_ptr(),
-        plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale, h_begin, nh)
+        plan.nq, plan.nb, plan.k_rows, Hq, Hkv, scale, h_begin, nh,
+        schedule.items.data_ptr() if schedule is not None else None,
+        part_o.data_ptr() if part_o is not None else None,
+        part_ml.data_ptr() if part_ml is not None else None,
+        schedule.n_items if schedule is not None else 0, 0)
     _lib.call("bam_attn_fwd", p)
+    if schedule is not None and schedule.combine.shape[0]:
+        _lib.call("bam_attn_fwd_combine", p, schedule.combine.data_ptr(),
+                  int(schedule.combine.shape[0]))
     return o, lse
 
 

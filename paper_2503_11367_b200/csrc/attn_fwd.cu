@@ -42,6 +42,29 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* m, uint64_t* bar, u
   tma_load_3d(m, bar, dst + kTileBytes / 2, 64, head, row0);
 }
 
+// One CTA's work: a whole query-block row (items == NULL: heavy-first order)
+// or a split-KV subblock [first, end) of its tile list (LPT-ordered items).
+struct WorkItem {
+  int j, n, slot;
+  const int32_t* tiles;
+};
+__device__ __forceinline__ WorkItem work_item(const BamAttnFwdParams& p, int y) {
+  WorkItem w;
+  if (p.items) {
+    const int4 it = reinterpret_cast<const int4*>(p.items)[y];
+    w.j = it.x;
+    w.tiles = p.row_tiles + p.row_off[it.x] + it.y;
+    w.n = it.z - it.y;
+    w.slot = it.w;
+  } else {
+    w.j = p.order ? p.order[y] : y;
+    w.tiles = p.row_tiles + p.row_off[w.j];
+    w.n = p.row_off[w.j + 1] - p.row_off[w.j];
+    w.slot = -1;
+  }
+  return w;
+}
+
 #ifndef BAM_FWD_POLY_EVERY
 #define BAM_FWD_POLY_EVERY 2
 #endif
@@ -71,7 +94,7 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
                                              uint32_t colS, uint32_t colO, uint64_t* bar_s_full,
                                              uint64_t* bar_p_ready, uint64_t* bar_pv_done, int j,
                                              int h, uint32_t warp, uint32_t lane,
-                                             const int32_t* tiles, int n) {
+                                             const int32_t* tiles, int n, int slot) {
   const int r = (warp & 3) * 32 + lane;
   const uint32_t lane_base = ((warp & 3) * 32) << 16;
   const long long qg = (long long)p.q_gid[j] * 128 + r;
@@ -154,6 +177,30 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
     tc_fence_before();
     mbar_arrive(bar_p_ready);
   }
+  // epilogue of a split-KV subblock: unnormalised fp32 O and (m, l) for the combine
+  if (slot >= 0) {
+    float* po = p.part_o + (((int64_t)slot * p.Hq + h) * 128 + r) * 128;
+    if (n > 0) {
+      mbar_wait_sleep(bar_pv_done, (n - 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rr[32];
+        BAM_TMEM_LD32(tmem + lane_base + colO + c * 32, rr);
+        tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(po + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(__uint_as_float(rr[4 * i]), __uint_as_float(rr[4 * i + 1]),
+                               __uint_as_float(rr[4 * i + 2]), __uint_as_float(rr[4 * i + 3]));
+      }
+    } else {
+      for (int i = 0; i < 32; ++i) reinterpret_cast<float4*>(po)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    reinterpret_cast<float2*>(p.part_ml)[((int64_t)slot * p.Hq + h) * 128 + r] =
+        make_float2(n > 0 ? m : -INFINITY, n > 0 ? l : 0.f);
+    return;
+  }
   // epilogue: O / l -> bf16, LSE
   const int64_t Tq = (int64_t)p.nq * 128;
   const int64_t row = (int64_t)j * 128 + r;
@@ -195,10 +242,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
   const int h = p.h_begin + blockIdx.x;
-  const int j = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
+  const WorkItem wi = work_item(p, blockIdx.y);
+  const int j = wi.j, n = wi.n, slot = wi.slot;
+  const int32_t* tiles = wi.tiles;
   const int hkv = (h - p.h_begin) / (nh / p.Hkv);
-  const int t0 = p.row_off[j], n = p.row_off[j + 1] - t0;
-  const int32_t* tiles = p.row_tiles + t0;
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.bar_q, 1);
@@ -279,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   } else {
     // ------------------------------------------------------------ softmax warps 0-3
     softmax_role(p, tmem, kColS, kColO, &sm.bar_s_full, &sm.bar_p_full, &sm.bar_pv_done, j, h,
-                 warp, lane, tiles, n);
+                 warp, lane, tiles, n, slot);
   }
   tc_fence_before();
   __syncthreads();
@@ -317,10 +364,10 @@ __global__ void __maxnreg__(168)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
   const int h0 = p.h_begin + 2 * blockIdx.x;
-  const int j = p.order ? p.order[blockIdx.y] : (int)blockIdx.y;
+  const WorkItem wi = work_item(p, blockIdx.y);
+  const int j = wi.j, n = wi.n, slot = wi.slot;
+  const int32_t* tiles = wi.tiles;
   const int hkv = (h0 - p.h_begin) / (nh / p.Hkv);
-  const int t0 = p.row_off[j], n = p.row_off[j + 1] - t0;
-  const int32_t* tiles = p.row_tiles + t0;
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B needs 1024-B alignment
@@ -430,7 +477,7 @@ __global__ void __maxnreg__(168)
     // ------------------------------------------------------------ softmax warpgroups
     const int i = warp >> 2;  // tile 0: warps 0-3, tile 1: warps 4-7
     softmax_role(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i], &sm.bar_p_ready[i],
-                 &sm.bar_pv_done[i], j, h0 + i, warp, lane, tiles, n);
+                 &sm.bar_pv_done[i], j, h0 + i, warp, lane, tiles, n, slot);
   }
   tc_fence_before();
   __syncthreads();
@@ -440,10 +487,68 @@ __global__ void __maxnreg__(168)
   }
 }
 
+// Aggregation kernel: merge the split-KV subblock partials
+// of a query block; one CTA per (combine record, head), thread = row.
+__global__ void __launch_bounds__(128) combine_kernel(const BamAttnFwdParams p,
+                                                      const int4* __restrict__ combine) {
+  const int4 c = combine[blockIdx.x];
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  const int h = p.h_begin + blockIdx.y;
+  if (blockIdx.y >= nh) return;
+  const int r = threadIdx.x;
+  const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
+  float M = -INFINITY;
+  for (int q = 0; q < c.z; ++q) M = fmaxf(M, ml[((int64_t)(c.y + q) * p.Hq + h) * 128 + r].x);
+  const float mb = M == -INFINITY ? 0.f : M;
+  float L = 0.f;
+  float acc[128];
+#pragma unroll
+  for (int d = 0; d < 128; ++d) acc[d] = 0.f;
+  for (int q = 0; q < c.z; ++q) {
+    const int64_t base = ((int64_t)(c.y + q) * p.Hq + h) * 128 + r;
+    const float2 v = ml[base];
+    const float w = ex2(v.x - mb);
+    L += w * v.y;
+    const float4* po = reinterpret_cast<const float4*>(p.part_o + base * 128);
+#pragma unroll
+    for (int d4 = 0; d4 < 32; ++d4) {
+      const float4 o = po[d4];
+      acc[4 * d4] = fmaf(w, o.x, acc[4 * d4]);
+      acc[4 * d4 + 1] = fmaf(w, o.y, acc[4 * d4 + 1]);
+      acc[4 * d4 + 2] = fmaf(w, o.z, acc[4 * d4 + 2]);
+      acc[4 * d4 + 3] = fmaf(w, o.w, acc[4 * d4 + 3]);
+    }
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  const int64_t row = (int64_t)c.x * 128 + r;
+  uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) +
+                                        (row * p.Hq + h) * 128);
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    dst[i] = make_uint4(pack_bf16(acc[8 * i] * inv, acc[8 * i + 1] * inv),
+                        pack_bf16(acc[8 * i + 2] * inv, acc[8 * i + 3] * inv),
+                        pack_bf16(acc[8 * i + 4] * inv, acc[8 * i + 5] * inv),
+                        pack_bf16(acc[8 * i + 6] * inv, acc[8 * i + 7] * inv));
+  p.lse[(int64_t)h * p.nq * 128 + row] =
+      L > 0.f ? (M + __log2f(L)) * 0.6931471805599453f : -INFINITY;
+}
+
 }  // namespace fwd
 }  // namespace bam
 
 using namespace bam;
+
+extern "C" int bam_attn_fwd_combine(const BamAttnFwdParams* pp, const int32_t* combine,
+                                    int32_t n_combine, void* stream) {
+  BAM_CHECK_ARG(pp != nullptr && combine != nullptr && n_combine >= 0,
+                "bam_attn_fwd_combine: bad arguments");
+  if (n_combine == 0) return kOk;
+  const int nh = pp->nh > 0 ? pp->nh : pp->Hq;
+  fwd::combine_kernel<<<dim3(n_combine, nh), 128, 0, (cudaStream_t)stream>>>(
+      *pp, reinterpret_cast<const int4*>(combine));
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
 
 extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
   BAM_CHECK_ARG(pp != nullptr, "bam_attn_fwd: null params");
@@ -466,14 +571,14 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
     const int smem = (int)sizeof(fwd::PairSmem);
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_pair_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid(nh / 2, p.nq);
+    dim3 grid(nh / 2, p.items ? p.n_items : p.nq);
     fwd::attn_fwd_pair_kernel<<<grid, fwd::kPairThreads, smem, (cudaStream_t)stream>>>(mq, mk,
                                                                                        mv, p);
   } else {
     const int smem = (int)sizeof(fwd::Smem) + 1024;
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid(nh, p.nq);
+    dim3 grid(nh, p.items ? p.n_items : p.nq);
     fwd::attn_fwd_kernel<<<grid, fwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, p);
   }
   BAM_LAUNCH_CHECK();

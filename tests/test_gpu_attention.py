@@ -170,3 +170,29 @@ def test_repeat_bitwise_deterministic(cfg_id):
         else:
             for name, a, b in zip(("O", "LSE", "dK", "dV"), cur, ref):
                 assert torch.equal(a, b), f"{name} differs between identical runs (race?)"
+
+
+@pytest.mark.parametrize("subblock", [1, 3, 8])
+def test_split_kv_schedule_matches_whole_rows(subblock):
+    """Intra-GPU subblocks (split-KV + aggregation kernel) must reproduce the
+    whole-row forward (fp32 partial merge: within bf16 rounding)."""
+    from paper_2503_11367_b200 import attention as A, mask as M
+
+    for Hq, Hkv in ((4, 2), (2, 2)):     # GQA pair kernel and the MHA kernel
+        mask = M.build_bitfield([("text", 300), ("img0", 256), ("text", 500), ("img1", 200),
+                                 ("text", 280)])
+        plan = A.plan_for_mask(mask)
+        T, dev = len(mask), torch.device("cuda")
+        g = torch.Generator(device=dev).manual_seed(7)
+        q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+        k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+        v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+        o, lse = A.attn_forward(q, k, v, plan)
+        sched = A.build_split_schedule(plan, subblock)
+        o2, lse2 = A.attn_forward(q, k, v, plan, schedule=sched)
+        assert (o2.float() - o.float()).abs().max().item() < 1e-2
+        assert (lse2 - lse).abs().max().item() < 1e-3
+        # the schedule is the reference split_block / LPT piece order
+        sizes = (sched.items[:, 2] - sched.items[:, 1]).cpu().tolist()
+        assert sizes == sorted(sizes, reverse=True)
+        assert max(sizes) <= subblock
