@@ -35,11 +35,15 @@ namespace bwd {
 constexpr int kThreads = 448;
 // warp roles
 constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
-// dQ^T tiles leave through one 32-KB TMA bulk reduce-add per step (staged in
-// shared memory) instead of 64 per-thread reductions; costs one Q/dO stage.
-#ifndef BAM_DQ_BULK
-#define BAM_DQ_BULK 1
+// How dQ^T tiles reach the fp32 accumulator:
+//   0: 64 per-thread red.global.add.f32 per step (one 128-B row segment per warp op)
+//   1: staged in shared memory, one 32-KB TMA bulk reduce-add (costs a Q/dO stage)
+//   2: 4x4 quad transposes in registers, 16 red.global.add.v4.f32 per thread
+//      (512 B per warp op, no shared-memory traffic)
+#ifndef BAM_DQ_MODE
+#define BAM_DQ_MODE 1
 #endif
+#define BAM_DQ_BULK (BAM_DQ_MODE == 1)
 constexpr int kStages = BAM_DQ_BULK ? 3 : 4;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
 constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
@@ -67,6 +71,29 @@ struct Smem {
 
 __device__ __forceinline__ void red_add(float* addr, float a) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
+}
+
+// v[i] = dQ[row0 + i][d] for this lane's column d.  Quads of lanes transpose
+// 4x4 blocks so lane 4m+k holds dQ[q][4m'..4m'+3] for q = row0 + 4t + k, then
+// one 16-B reduction per (t): a warp covers 4 rows x 128 B per instruction.
+__device__ __forceinline__ void red_add_quads(float* base, int d, const uint32_t (&v)[32],
+                                              int row0) {
+  const int k = d & 3, col = (d & ~3) ;   // col: first column of this lane's quad
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    float x0 = __uint_as_float(v[4 * t]), x1 = __uint_as_float(v[4 * t + 1]);
+    float x2 = __uint_as_float(v[4 * t + 2]), x3 = __uint_as_float(v[4 * t + 3]);
+    float s0 = __shfl_xor_sync(0xffffffffu, (k & 1) ? x0 : x1, 1);
+    float s1 = __shfl_xor_sync(0xffffffffu, (k & 1) ? x2 : x3, 1);
+    if (k & 1) { x0 = s0; x2 = s1; } else { x1 = s0; x3 = s1; }
+    s0 = __shfl_xor_sync(0xffffffffu, (k & 2) ? x0 : x2, 2);
+    s1 = __shfl_xor_sync(0xffffffffu, (k & 2) ? x1 : x3, 2);
+    if (k & 2) { x0 = s0; x1 = s1; } else { x2 = s0; x3 = s1; }
+    float* addr = base + (int64_t)(row0 + 4 * t + k) * 128 + col;
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "f"(x0), "f"(x1),
+                 "f"(x2), "f"(x3)
+                 : "memory");
+  }
 }
 
 // dst[(kRow0 + i) * 128] += v[i] for i < 32, rows 512 B apart (immediate offsets)
@@ -432,6 +459,9 @@ __global__ void __maxnreg__(128)
             "r"(smem_u32(sm.dq_stage)), "n"(64 * 128 * 4)
             : "memory");
       }
+#elif BAM_DQ_MODE == 2
+      red_add_quads(dst - d, d, a, 0);
+      red_add_quads(dst - d, d, c2, 32);
 #else
       red_add_rows<0>(dst, a);
       red_add_rows<32>(dst, c2);
