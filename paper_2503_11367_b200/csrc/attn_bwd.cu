@@ -44,11 +44,24 @@ constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
 #define BAM_DQ_MODE 1
 #endif
 #define BAM_DQ_BULK (BAM_DQ_MODE == 1)
-constexpr int kStages = BAM_DQ_BULK ? 3 : 4;
+// 1: K and V resident in TMEM as the A operands of S^T / dP^T (TS MMAs), dK from
+// dS^T in shared memory: per step the MMAs read 128 KB of shared memory instead
+// of 176 KB (an SS MMA with N = 64 is shared-memory bound at 48 clk per k-step,
+// a TS one runs at the 32-clk tensor rate: tools/mma_bench.cu), at the price of
+// single-buffered S / dP, which puts the softmax / dS work on the MMA chain.
+// Measured on config 4: MMA pipeline alone 1600 vs 1240 TFLOP/s, full kernel
+// 915 vs 955 TFLOP/s, both bounded by the dQ reduce-add traffic into L2
+// (DESIGN.md "Backward bounds").  0 (default) = double-buffered, S / dP SS.
+#ifndef BAM_BWD_KVT
+#define BAM_BWD_KVT 0
+#endif
+constexpr int kStages = (BAM_DQ_BULK && !BAM_BWD_KVT) ? 3 : 4;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
 constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
 constexpr uint32_t kDsBytes = 128 * 64 * 2;      // dS^T: 128 key rows x 64 query cols
 constexpr uint32_t kColDV = 0, kColDK = 128, kColBuf = 256;  // buffer b: S at 256+128b, dP at +64
+// BAM_BWD_KVT: K, V bf16 pairs (64 columns each), then the single S and dP/dQ^T buffers
+constexpr uint32_t kColK = 256, kColV = 320, kColS = 384, kColDP = 448;
 
 struct Stage {
   alignas(1024) uint8_t q[kHalfBytes];
@@ -58,14 +71,15 @@ struct Stage {
 struct Smem {
   alignas(1024) uint8_t k[kTileBytes];
   alignas(1024) uint8_t v[kTileBytes];
-  alignas(1024) uint8_t ds[2][kDsBytes];
+  alignas(1024) uint8_t ds[BAM_BWD_KVT ? 1 : 2][kDsBytes];
   Stage st[kStages];
-#if BAM_DQ_BULK
+#if BAM_DQ_BULK && !BAM_BWD_KVT
   alignas(128) float dq_stage[64 * 128];  // dQ tile [64 queries][128 d] fp32 for the bulk reduce
 #endif
   alignas(16) float ld[kStages][128];   // per stage: (lse * log2e, delta) pairs, 64 queries
   uint64_t bar_kv, bar_full[kStages], bar_empty[kStages];
   uint64_t bar_sdp_full[2], bar_p_ready[2], bar_mma_done[2], bar_dq_full[2], bar_dq_empty[2];
+  uint64_t bar_kvt, bar_dp_full, bar_ds_ready;  // BAM_BWD_KVT (S(s) done = bar_sdp_full[0])
   uint32_t tmem_base;
 };
 
@@ -106,6 +120,16 @@ __device__ __forceinline__ void red_add_rows(float* dst, const uint32_t (&v)[32]
     red_add_rows<kRow0, i + 1>(dst, v);
   }
 }
+
+// Development aid: -DBAM_EXPERIMENT_MMA_ONLY runs only the TMA + MMA pipeline
+// (no softmax / dQ work, garbage results) to measure the operand-feed bound.
+#ifdef BAM_EXPERIMENT_MMA_ONLY
+#define BAM_XWAIT(bar, ph) ((void)0)
+constexpr bool kMmaOnly = true;
+#else
+#define BAM_XWAIT(bar, ph) mbar_wait(bar, ph)
+constexpr bool kMmaOnly = false;
+#endif
 
 struct StepInfo {
   int h, jq, cls, half;
@@ -176,6 +200,9 @@ __global__ void __maxnreg__(128)
       mbar_init(&sm.bar_dq_full[b], 1);
       mbar_init(&sm.bar_dq_empty[b], 128);
     }
+    mbar_init(&sm.bar_kvt, 256);
+    mbar_init(&sm.bar_dp_full, 1);
+    mbar_init(&sm.bar_ds_ready, 256);
     fence_mbar_init();
   }
   if (warp == kWarpMMA) {
@@ -247,6 +274,74 @@ __global__ void __maxnreg__(128)
       const uint64_t d_ds0 = sdesc_sw128(smem_u32(sm.ds[0]), 16, 1024);
       constexpr uint32_t kStage16 = sizeof(Stage) >> 4, kDo16 = kHalfBytes >> 4;
       constexpr uint32_t kDs16 = kDsBytes >> 4;
+#if BAM_BWD_KVT
+      (void)dk_k; (void)dk_v; (void)kDs16;
+      const uint32_t tK = tmem + kColK, tV = tmem + kColV, tS = tmem + kColS, tDP = tmem + kColDP;
+      mbar_wait(&sm.bar_kvt, 0);  // K / V rows stored into TMEM by the compute warps
+      // S^T(s) = K Q^T (A = K from TMEM) -> S; S(s) overwrites P^T(s-1), the A operand of
+      // dV(s-1): issued earlier by this thread, and tcgen05.mma ops execute in issue order.
+      auto issue_s = [&](int s) {
+        const int st = s % kStages;
+        mbar_wait(&sm.bar_full[st], (s / kStages) & 1);
+        BAM_TRACE_EV(trace_cta && leader, 11, s);
+        tc_fence_after();
+        const uint64_t dq = d_q0 + st * kStage16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
+          mma_ts_w(tS, tK + 8 * kk, dq + kq, id_s, kk > 0, leader);
+        }
+        tc_commit_w(&sm.bar_sdp_full[0], leader);
+      };
+      // dP^T(s) = V dO^T (A = V from TMEM) -> dP, once dQ^T(s-1) has been drained from it
+      auto issue_dp = [&](int s) {
+        const int st = s % kStages;
+        if (s > 0) BAM_XWAIT(&sm.bar_dq_empty[0], (s - 1) & 1);
+        BAM_TRACE_EV(trace_cta && leader, 1, s);
+        tc_fence_after();
+        const uint64_t ddo = d_q0 + st * kStage16 + kDo16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
+          mma_ts_w(tDP, tV + 8 * kk, ddo + kq, id_s, kk > 0, leader);
+        }
+        tc_commit_w(&sm.bar_dp_full, leader);
+        BAM_TRACE_EV(trace_cta && leader, 12, s);
+      };
+      issue_s(0);
+      issue_dp(0);
+      for (int s = 0; s < nsteps; ++s) {
+        const int st = s % kStages;
+        const uint32_t ph = s & 1;
+        const uint64_t dqmn = d_q0mn + st * kStage16, ddomn = dqmn + kDo16;
+        BAM_XWAIT(&sm.bar_p_ready[0], ph);
+        BAM_TRACE_EV(trace_cta && leader, 2, s);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO  (A = P^T bf16 in the S columns)
+          mma_ts_w(tmem + kColDV, tS + (kk >> 1) * 32 + (kk & 1) * 8, ddomn + kk * 128, id_kv,
+                   (s > 0 || kk > 0), leader);
+        if (s + 1 < nsteps) issue_s(s + 1);  // overlaps the compute warps' dS(s)
+        BAM_XWAIT(&sm.bar_ds_ready, ph);
+        BAM_TRACE_EV(trace_cta && leader, 14, s);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q  (A = dS^T K-major in shared memory)
+          mma_ss_w(tmem + kColDK, d_ds0 + 2 * kk, dqmn + kk * 128, id_kv, (s > 0 || kk > 0),
+                   leader);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T -> the dP columns
+          mma_ss_w(tDP, dk_kmn + kk * 128, d_ds0 + kk * 128, id_q, kk > 0, leader);
+        tc_commit_w(&sm.bar_dq_full[0], leader);
+        if (shared)
+          tc_commit_mc_w(&sm.bar_empty[st], 0x3, leader);
+        else
+          tc_commit_w(&sm.bar_empty[st], leader);
+        BAM_TRACE_EV(trace_cta && leader, 3, s);
+        if (s + 1 < nsteps) issue_dp(s + 1);
+      }
+      tc_commit_w(&sm.bar_mma_done[0], leader);
+#else
       auto issue_sdp = [&](int s) {
         const int st = s % kStages, b = s & 1;
         mbar_wait(&sm.bar_full[st], (s / kStages) & 1);
@@ -265,7 +360,7 @@ __global__ void __maxnreg__(128)
           mma_ss_w(tS, dk_k + ka, dq + kq, id_s, kk > 0, leader);
         }
         BAM_TRACE_EV(trace_cta && leader, 12, s);
-        if (s >= 2) mbar_wait(&sm.bar_dq_empty[b], ((s >> 1) - 1) & 1);  // dQ^T(s-2) drained
+        if (s >= 2) BAM_XWAIT(&sm.bar_dq_empty[b], ((s >> 1) - 1) & 1);  // dQ^T(s-2) drained
         BAM_TRACE_EV(trace_cta && leader, 1, s);
         tc_fence_after();
 #pragma unroll
@@ -285,7 +380,7 @@ __global__ void __maxnreg__(128)
         const uint64_t dqmn = d_q0mn + st * kStage16, ddomn = dqmn + kDo16;
         const uint64_t dds = d_ds0 + b * kDs16;
         const uint32_t tS = tmem + kColBuf + 128 * b, tDQ = tS + 64;
-        mbar_wait(&sm.bar_p_ready[b], (s >> 1) & 1);
+        BAM_XWAIT(&sm.bar_p_ready[b], (s >> 1) & 1);
         BAM_TRACE_EV(trace_cta && leader, 2, s);
         tc_fence_after();
         // dV += P^T dO   (K = 64 queries: 4 steps of 16 rows = 2048 B)
@@ -313,6 +408,7 @@ __global__ void __maxnreg__(128)
         tc_commit_w(&sm.bar_mma_done[b], leader);
         BAM_TRACE_EV(trace_cta && leader, 3, s);
       }
+#endif
     }
   } else if (warp < kWarpDQ) {
     // ------------------------------------------------------------ compute warps 0-7
@@ -325,7 +421,99 @@ __global__ void __maxnreg__(128)
     const long long dk = p.desc[kg];
     const float scale_log2 = p.scale * 1.4426950408889634f;
     StepIter it(col, grp, hkv, p.h_begin);
-    for (int s = 0; s < nsteps; ++s) {
+#if BAM_BWD_KVT
+    if (nsteps > 0) {
+      // Row r of K (warpgroup 0) / V (warpgroup 1) from the swizzled tile into
+      // TMEM lane r as bf16 pairs: column j = head-dim elements 2j, 2j+1.
+      mbar_wait_sleep(&sm.bar_kv, 0);
+      const uint8_t* src = (c == 0 ? sm.k : sm.v) + r * 128;
+#pragma unroll
+      for (int hb = 0; hb < 2; ++hb) {
+        uint32_t w[32];
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const uint4 x = *reinterpret_cast<const uint4*>(src + hb * (kTileBytes / 2) +
+                                                          ((ch ^ (r & 7)) << 4));
+          w[4 * ch] = x.x;
+          w[4 * ch + 1] = x.y;
+          w[4 * ch + 2] = x.z;
+          w[4 * ch + 3] = x.w;
+        }
+        BAM_TMEM_ST32(tmem + lane_base + (c == 0 ? kColK : kColV) + 32 * hb, w);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm.bar_kvt);
+    }
+    for (int s = 0; s < (kMmaOnly ? 0 : nsteps); ++s) {
+      const int st = s % kStages;
+      const uint32_t ph = s & 1;
+      const StepInfo si = it.get();
+      it.next();
+      const uint32_t tS = tmem + kColS + lane_base, tdP = tmem + kColDP + lane_base;
+      const uint32_t ds_row = smem_u32(sm.ds[0]) + r * 128;
+      mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_sdp_full[0], ph);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 4, s);
+      tc_fence_after();
+      uint32_t sr[32];
+      BAM_TMEM_LD32(tS + c * 32, sr);
+      uint32_t allow = si.cls ? 0xFFFFFFFFu : 0u;
+      if (si.cls == 2) {
+        const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64 + c * 32;
+        allow = 0;
+#pragma unroll 1
+        for (int i = 0; i < 32; ++i)
+          allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
+      }
+      tmem_wait_ld();
+      const float4* ld = reinterpret_cast<const float4*>(sm.ld[st] + c * 64);  // (lse*log2e, D)
+      {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          const float4 v = ld[i2];
+          float p0 = ex2(fmaf(__uint_as_float(sr[2 * i2]), scale_log2, -v.x));
+          float p1 = ex2(fmaf(__uint_as_float(sr[2 * i2 + 1]), scale_log2, -v.z));
+          p0 = (allow >> (2 * i2)) & 1 ? p0 : 0.f;
+          p1 = (allow >> (2 * i2 + 1)) & 1 ? p1 : 0.f;
+          sr[2 * i2] = __float_as_uint(p0);
+          sr[2 * i2 + 1] = __float_as_uint(p1);
+          pk[i2] = pack_bf16(p0, p1);
+        }
+        BAM_TMEM_ST16(tS + c * 32, pk);  // P^T over this warpgroup's own S columns
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm.bar_p_ready[0]);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 5, s);
+      mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_dp_full, ph);
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 6, s);
+      tc_fence_after();
+      uint32_t dr[32], dsk[16];
+      BAM_TMEM_LD32(tdP + c * 32, dr);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i2 = 0; i2 < 16; ++i2) {
+        const float4 v = ld[i2];
+        dsk[i2] = pack_bf16(__uint_as_float(sr[2 * i2]) * (__uint_as_float(dr[2 * i2]) - v.y),
+                            __uint_as_float(sr[2 * i2 + 1]) * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
+      }
+      // dS^T row r, query columns 32c .. 32c+31 (the A operand of dK, B of dQ^T)
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint32_t chunk = (uint32_t)(c * 4 + q4) ^ (uint32_t)(r & 7);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ds_row + chunk * 16),
+                     "r"(dsk[q4 * 4]), "r"(dsk[q4 * 4 + 1]), "r"(dsk[q4 * 4 + 2]),
+                     "r"(dsk[q4 * 4 + 3])
+                     : "memory");
+      }
+      fence_async_smem();
+      tc_fence_before();
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 7, s);
+      mbar_arrive(&sm.bar_ds_ready);
+    }
+#else
+    for (int s = 0; s < (kMmaOnly ? 0 : nsteps); ++s) {
       const int st = s % kStages, b = s & 1;
       const StepInfo si = it.get();
       it.next();
@@ -385,6 +573,7 @@ __global__ void __maxnreg__(128)
       BAM_TRACE_EV(trace_cta && threadIdx.x == 128, 7, s);
       mbar_arrive(&sm.bar_p_ready[b]);
     }
+#endif
     // epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled), fp32 rows
     if (kb < 0) goto done;  // padding slot of the last cluster
     {
@@ -392,7 +581,11 @@ __global__ void __maxnreg__(128)
     float* dst = (c == 0 ? p.dv : p.dk) + (row * p.Hkv + hkv) * 128;
     const float mul = c == 0 ? 1.f : p.scale;
     if (nsteps > 0) {
+#if BAM_BWD_KVT
+      mbar_wait_sleep(&sm.bar_mma_done[0], 0);
+#else
       mbar_wait_sleep(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
+#endif
       tc_fence_after();
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
@@ -420,13 +613,25 @@ __global__ void __maxnreg__(128)
     const int d = (warp - kWarpDQ) * 32 + lane;
     const uint32_t lane_base = ((warp - kWarpDQ) * 32) << 16;
     StepIter it(col, grp, hkv, p.h_begin);
-    for (int s = 0; s < nsteps; ++s) {
+#if BAM_DQ_BULK
+#if BAM_BWD_KVT
+    float* const dq_stage = reinterpret_cast<float*>(sm.v);  // V lives in TMEM by now
+#else
+    float* const dq_stage = sm.dq_stage;
+#endif
+#endif
+    for (int s = 0; s < (kMmaOnly ? 0 : nsteps); ++s) {
+#if BAM_BWD_KVT
+      const int b = 0;
+      const uint32_t tDQ = tmem + kColDP, dq_par = s & 1;
+#else
       const int b = s & 1;
+      const uint32_t tDQ = tmem + kColBuf + 128 * b + 64, dq_par = (s >> 1) & 1;
+#endif
       const StepInfo si = it.get();
-        it.next();
+      it.next();
       float* dst = p.dq_acc + ((int64_t)si.h * Tq + si.jq * 128 + si.half * 64) * 128 + d;
-      const uint32_t tDQ = tmem + kColBuf + 128 * b + 64;
-      mbar_wait_sleep(&sm.bar_dq_full[b], (s >> 1) & 1);
+      mbar_wait_sleep(&sm.bar_dq_full[b], dq_par);
       BAM_TRACE_EV(trace_cta && threadIdx.x == kWarpDQ * 32, 8, s);
       tc_fence_after();
       uint32_t a[32], c2[32];
@@ -444,19 +649,21 @@ __global__ void __maxnreg__(128)
       // staging buffer free once the previous bulk reduce has read it
       const bool dq_leader = threadIdx.x == kWarpDQ * 32;
       if (dq_leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      BAM_TRACE_EV(trace_cta && dq_leader, 13, s);
       named_bar_sync(1, 128);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) sm.dq_stage[i * 128 + d] = __uint_as_float(a[i]);
+      for (int i = 0; i < 32; ++i) dq_stage[i * 128 + d] = __uint_as_float(a[i]);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) sm.dq_stage[(32 + i) * 128 + d] = __uint_as_float(c2[i]);
+      for (int i = 0; i < 32; ++i) dq_stage[(32 + i) * 128 + d] = __uint_as_float(c2[i]);
       fence_async_smem();
       named_bar_sync(1, 128);
+      BAM_TRACE_EV(trace_cta && dq_leader, 15, s);
       if (dq_leader) {
         float* gdst = dst - d;   // 64 rows x 512 B contiguous in the head-major accumulator
         asm volatile(
             "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n\t"
             "cp.async.bulk.commit_group;" ::"l"(gdst),
-            "r"(smem_u32(sm.dq_stage)), "n"(64 * 128 * 4)
+            "r"(smem_u32(dq_stage)), "n"(64 * 128 * 4)
             : "memory");
       }
 #elif BAM_DQ_MODE == 2
