@@ -220,7 +220,7 @@ def main():
     k = torch.randn(T, Hkv, D, device=dev, generator=gen, dtype=torch.bfloat16)
     v = torch.randn(T, Hkv, D, device=dev, generator=gen, dtype=torch.bfloat16)
     do = torch.randn(T, Hq, D, device=dev, generator=gen, dtype=torch.bfloat16)
-    q_loc, k_loc, v_loc, do_loc = (CP.shard_rows(t, layout).contiguous() for t in (q, k, v, do))
+    q_loc, k_loc, v_loc, do_loc = CP.shard_rows(q, k, v, do, layout=layout)  # one permute launch
     del q, k, v, do
     # local share of the algorithmic FLOP (for the per-kernel roofline)
     rows_allowed = None

@@ -217,6 +217,19 @@ int bam_build_pair_lists(const int32_t* col_off, const int32_t* col_tiles, const
                          int32_t nb, int32_t* slot_kb, int32_t* slot_cnt, int32_t* slot_off,
                          int32_t* slot_tiles, int32_t* pair_shared, void* stream);
 
+/* ---- token permutation ----------------- */
+/* The CP runtime permutes tokens into the LPT block layout before attention
+ * and back afterwards.  Block-row gather / scatter for up to BAM_PERMUTE_MAX
+ * tensors in one launch: a block is block_rows rows of row_bytes[t] bytes.
+ *   scatter == 0 (gather):  dst[t] block i      = src[t] block idx[i]
+ *   scatter != 0 (scatter): dst[t] block idx[i] = src[t] block i
+ * for i < n_blocks.  Pointers and row_bytes must be 16-byte aligned; idx is a
+ * device array; src / dst are device pointers (HOST arrays of them). */
+#define BAM_PERMUTE_MAX 4
+int bam_permute_blocks(const void* const* src, void* const* dst, const int64_t* row_bytes,
+                       int32_t n_tensors, const int32_t* idx, int32_t n_blocks,
+                       int32_t block_rows, int32_t scatter, void* stream);
+
 /* fp32 -> bf16 conversion (dk/dv partials to the bf16 gradient layout). */
 int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 

@@ -24,11 +24,13 @@ of group g overlaps the backward kernel of group g+1.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from . import attention as A
 from . import balance as B
 from .mask import BitfieldMask, classify_device
@@ -70,11 +72,48 @@ def cp_layout(owner: torch.Tensor, world: int, rank: int) -> CPLayout:
                     k_row=k_row, counts=counts, max_blocks=max_blocks)
 
 
-def shard_rows(x: torch.Tensor, layout: CPLayout) -> torch.Tensor:
-    """Rows of this rank's blocks from a full-sequence [T, H, d] tensor."""
-    idx = (layout.local_blocks.to(torch.int64)[:, None] * BLOCK +
-           torch.arange(BLOCK, device=layout.local_blocks.device)[None, :]).reshape(-1)
-    return x.index_select(0, idx.to(x.device))
+def permute_blocks(srcs, dsts, idx: torch.Tensor, scatter: bool = False) -> None:
+    """Token permutation with ``bam_permute_blocks``: for
+    every (src, dst) pair, gather (dst block i = src block idx[i]) or scatter
+    (dst block idx[i] = src block i) 128-row blocks, all tensors in one launch.
+    Tensors are contiguous CUDA tensors whose rows are 16-byte multiples."""
+    srcs, dsts = list(srcs), list(dsts)
+    if not 1 <= len(srcs) == len(dsts) <= 4:
+        raise ValueError("permute_blocks: 1..4 (src, dst) pairs")
+    _lib.require_cuda()
+    for t in srcs + dsts:
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("permute_blocks: tensors must be contiguous CUDA tensors "
+                             "(no CPU fallback)")
+    idx = idx.to(device=srcs[0].device, dtype=torch.int32).contiguous()
+    n = len(srcs)
+    row_bytes = [t[0].numel() * t.element_size() if t.shape[0] else 16 for t in srcs]
+    _lib.call("bam_permute_blocks", (ctypes.c_void_p * n)(*[t.data_ptr() for t in srcs]),
+              (ctypes.c_void_p * n)(*[t.data_ptr() for t in dsts]),
+              (ctypes.c_int64 * n)(*row_bytes), n, idx.data_ptr(), int(idx.numel()), BLOCK,
+              int(scatter))
+
+
+def shard_rows(*xs: torch.Tensor, layout: CPLayout = None):
+    """Rows of this rank's blocks (in ``layout.local_blocks`` order) from
+    full-sequence [T, ...] CUDA tensors: one fused gather launch for all of
+    them.  ``shard_rows(x, layout)`` returns one tensor, ``shard_rows(q, k,
+    v, layout=layout)`` a list."""
+    if layout is None and xs and isinstance(xs[-1], CPLayout):
+        xs, layout = xs[:-1], xs[-1]
+    xs = [x.contiguous() for x in xs]
+    outs = [torch.empty((layout.n_local * BLOCK,) + tuple(x.shape[1:]), dtype=x.dtype,
+                        device=x.device) for x in xs]
+    for i in range(0, len(xs), 4):
+        permute_blocks(xs[i:i + 4], outs[i:i + 4], layout.local_blocks)
+    return outs[0] if len(outs) == 1 else outs
+
+
+def unshard_rows(y_loc: torch.Tensor, layout: CPLayout, out: torch.Tensor) -> torch.Tensor:
+    """Inverse of ``shard_rows``: scatter this rank's rows back to their
+    sequence positions in the full [T, ...] tensor ``out`` (other rows kept)."""
+    permute_blocks([y_loc.contiguous()], [out], layout.local_blocks, scatter=True)
+    return out
 
 
 def pad_rows(x: torch.Tensor, layout: CPLayout) -> torch.Tensor:

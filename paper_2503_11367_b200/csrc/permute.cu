@@ -1,0 +1,79 @@
+// Token permutation around CP attention: block-row gather /
+// scatter of up to four tensors per launch.  Pure HBM streaming: every thread
+// moves 16-B vectors, four in flight, over a grid of 148 x 8 CTAs.
+#include "../../include/bam.h"
+#include "common.cuh"
+
+namespace bam {
+namespace perm {
+
+struct PermuteArgs {
+  const uint4* src[BAM_PERMUTE_MAX];
+  uint4* dst[BAM_PERMUTE_MAX];
+  int64_t row_vec[BAM_PERMUTE_MAX];   // 16-B vectors per row
+  int64_t total[BAM_PERMUTE_MAX];     // vectors per tensor = n_blocks * block_rows * row_vec
+  int32_t n_tensors;
+};
+
+__global__ void __launch_bounds__(256) permute_kernel(const PermuteArgs a,
+                                                      const int32_t* __restrict__ idx,
+                                                      int32_t block_rows, int32_t scatter) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int t = 0; t < a.n_tensors; ++t) {
+    const int64_t rv = a.row_vec[t], per_block = rv * block_rows, total = a.total[t];
+    const uint4* __restrict__ src = a.src[t];
+    uint4* __restrict__ dst = a.dst[t];
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total;
+         base += 4 * stride) {
+      uint4 v[4];
+      int64_t out[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = base + u * stride;
+        out[u] = -1;
+        if (e < total) {
+          const int64_t blk = e / per_block, within = e - blk * per_block;
+          const int64_t other = (int64_t)__ldg(idx + blk) * per_block + within;
+          v[u] = __ldg(src + (scatter ? e : other));
+          out[u] = scatter ? other : e;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (out[u] >= 0) dst[out[u]] = v[u];
+    }
+  }
+}
+
+}  // namespace perm
+}  // namespace bam
+
+using namespace bam;
+
+extern "C" int bam_permute_blocks(const void* const* src, void* const* dst,
+                                  const int64_t* row_bytes, int32_t n_tensors, const int32_t* idx,
+                                  int32_t n_blocks, int32_t block_rows, int32_t scatter,
+                                  void* stream) {
+  BAM_CHECK_ARG(n_tensors >= 1 && n_tensors <= BAM_PERMUTE_MAX && src && dst && row_bytes,
+                "bam_permute_blocks: n_tensors=%d (1..%d)", n_tensors, BAM_PERMUTE_MAX);
+  BAM_CHECK_ARG(n_blocks >= 0 && block_rows >= 1, "bam_permute_blocks: n_blocks=%d block_rows=%d",
+                n_blocks, block_rows);
+  if (n_blocks == 0) return kOk;
+  BAM_CHECK_ARG(idx != nullptr, "bam_permute_blocks: null idx");
+  perm::PermuteArgs a = {};
+  a.n_tensors = n_tensors;
+  for (int t = 0; t < n_tensors; ++t) {
+    BAM_CHECK_ARG(row_bytes[t] > 0 && row_bytes[t] % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(src[t]) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(dst[t]) & 15) == 0,
+                  "bam_permute_blocks: tensor %d needs 16-byte aligned rows / pointers "
+                  "(row_bytes=%lld)", t, (long long)row_bytes[t]);
+    a.src[t] = static_cast<const uint4*>(src[t]);
+    a.dst[t] = static_cast<uint4*>(dst[t]);
+    a.row_vec[t] = row_bytes[t] / 16;
+    a.total[t] = a.row_vec[t] * block_rows * (int64_t)n_blocks;
+  }
+  perm::permute_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a, idx, block_rows, scatter);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}

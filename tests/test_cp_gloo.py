@@ -57,7 +57,11 @@ def _worker(rank, world, port, policy, result_dir):
         k = torch.randn(T, Hkv, 128, generator=g)
         v = torch.randn(T, Hkv, 128, generator=g)
         do = torch.randn(T, Hq, 128, generator=g)
-        q_loc, k_loc, v_loc, do_loc = (cp.shard_rows(t, layout) for t in (q, k, v, do))
+        # the product's shard_rows is a CUDA kernel (tests/test_gpu_cp.py); here
+        # the same block-row gather by indexing, to feed the gloo collectives
+        rows = (layout.local_blocks.to(torch.int64)[:, None] * BLOCK +
+                torch.arange(BLOCK)[None, :]).reshape(-1)
+        q_loc, k_loc, v_loc, do_loc = (t.index_select(0, rows) for t in (q, k, v, do))
 
         k_all, v_all = cp.gather_kv(k_loc, v_loc, layout)
         assert k_all.shape[0] == world * layout.max_blocks * BLOCK

@@ -40,7 +40,7 @@ q = torch.randn(T, Hq, 128, generator=g).to(torch.bfloat16)
 k = torch.randn(T, Hkv, 128, generator=g).to(torch.bfloat16)
 v = torch.randn(T, Hkv, 128, generator=g).to(torch.bfloat16)
 do = torch.randn(T, Hq, 128, generator=g).to(torch.bfloat16)
-q_loc, k_loc, v_loc, do_loc = (cp.shard_rows(t.to(dev), lay).contiguous() for t in (q, k, v, do))
+q_loc, k_loc, v_loc, do_loc = cp.shard_rows(*(t.to(dev) for t in (q, k, v, do)), layout=lay)
 q_loc.requires_grad_(True)
 k_loc.requires_grad_(True)
 v_loc.requires_grad_(True)

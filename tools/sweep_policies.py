@@ -56,7 +56,7 @@ for name in masks:
     for pol in policies:
         plan = cp.make_cp_plan(desc, world, rank, pol)
         lay = plan.layout
-        ql, kl, vl, dol = (cp.shard_rows(t, lay).contiguous() for t in (q, k, v, do))
+        ql, kl, vl, dol = cp.shard_rows(q, k, v, do, layout=lay)
 
         def step(ev):
             k_all, v_all = cp.gather_kv(kl, vl, lay) if world > 1 else (kl, vl)
