@@ -65,31 +65,44 @@ __device__ __forceinline__ WorkItem work_item(const BamAttnFwdParams& p, int y) 
   return w;
 }
 
-#ifndef BAM_FWD_POLY_EVERY
-#define BAM_FWD_POLY_EVERY 2
+// One in kPolyEvery exponential PAIRS runs on the FMA pipe (ex2_poly2) so the MUFU
+// unit (16 ex2 / clk / SM) is not the softmax bottleneck.  Measured on B200:
+// the MHA kernel (two CTAs per SM) is fastest at 1 in 3, the GQA head-pair
+// kernel (two softmax warpgroups sharing each SM sub-partition's issue slots)
+// with none (config 4: 1090 vs 1040 TFLOP/s at 1 in 4).
+#ifndef BAM_FWD_POLY_MHA
+#define BAM_FWD_POLY_MHA 3
 #endif
-constexpr int kPolyEvery = BAM_FWD_POLY_EVERY;
+#ifndef BAM_FWD_POLY_PAIR
+#define BAM_FWD_POLY_PAIR 0
+#endif
 
-// 2^x on the FMA pipe: x = n + f, f in [-0.5, 0.5] (round via the 1.5*2^23
-// magic constant), 2^f by a degree-4 polynomial (rel. err < 4e-6, well below
-// bf16 P rounding), exponent n added to the float bits.  x <= 8 here (lazy
-// rescale); clamping at -127 makes 2^x flush to ~0 like ex2.approx.ftz.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float t = x + 12582912.f;                 // integer part in the low mantissa bits
-  const float f = x - (t - 12582912.f);           // [-0.5, 0.5]
-  float p = fmaf(1.3333558e-3f, f, 9.6181291e-3f);
-  p = fmaf(p, f, 5.5504109e-2f);
-  p = fmaf(p, f, 2.4022651e-1f);
-  p = fmaf(p, f, 6.9314718e-1f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+// 2^x for a pair on the FMA pipe (packed FFMA2): x = n + f, f in [-0.5, 0.5]
+// (round via the 1.5*2^23 magic constant), 2^f by a degree-4 polynomial
+// (rel. err < 4e-6, well below bf16 P rounding), exponent n added to the
+// float bits.  x <= 8 here (lazy rescale); clamping at -127 makes 2^x flush
+// to ~0 like ex2.approx.ftz.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.f;
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));  // integer part in the low bits
+  const float2 f = ffma2(fadd2(t, make_float2(-kMagic, -kMagic)), make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(1.3333558e-3f, 1.3333558e-3f), f,
+                   make_float2(9.6181291e-3f, 9.6181291e-3f));
+  p = ffma2(p, f, make_float2(5.5504109e-2f, 5.5504109e-2f));
+  p = ffma2(p, f, make_float2(2.4022651e-1f, 2.4022651e-1f));
+  p = ffma2(p, f, make_float2(6.9314718e-1f, 6.9314718e-1f));
+  p = ffma2(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 // Softmax / epilogue role of one 128-row query tile: thread (warp w, lane)
 // owns row r = 32 w + lane = TMEM lane r.  Per key tile t: wait S(t), mask
 // PARTIAL tiles, online softmax (log2 domain, lazy 2^8 rescale of O in TMEM),
 // P -> bf16 into the S columns, arrive p_ready.  Finally O / l -> bf16, LSE.
+template <int kPolyEvery>
 __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t tmem,
                                              uint32_t colS, uint32_t colO, uint64_t* bar_s_full,
                                              uint64_t* bar_p_ready, uint64_t* bar_pv_done, int j,
@@ -107,15 +120,10 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
     const long long kg0 = (long long)(e >> 2) * 128;
     mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(bar_s_full, t & 1);
     tc_fence_after();
-    float s[128];
+    uint32_t sr[128];  // S row as fp32 bits: four TMEM loads in flight, one wait
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t rr[32];
-      BAM_TMEM_LD32(tmem + lane_base + colS + c * 32, rr);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(rr[i]);
-    }
+    for (int c = 0; c < 4; ++c) BAM_TMEM_LD32(tmem + lane_base + colS + c * 32, (sr + c * 32));
+    tmem_wait_ld();
     if (cls == 2) {  // PARTIAL: descriptor predicate per element, 32 columns at a time
       const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
 #pragma unroll
@@ -128,12 +136,20 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (!((bits >> i) & 1)) s[c * 32 + i] = -INFINITY;
+          if (!((bits >> i) & 1)) sr[c * 32 + i] = 0xff800000u;  // -inf
       }
     }
-    float mt = -INFINITY;
+    // row max: eight independent FMNMX3 chains instead of one serial chain
+    float mx[8];
 #pragma unroll
-    for (int c = 0; c < 128; ++c) mt = fmaxf(mt, s[c]);
+    for (int k = 0; k < 8; ++k) mx[k] = fmaxf(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1]));
+#pragma unroll
+    for (int c = 16; c < 128; c += 16)
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
+    const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
     const float m_new = fmaxf(m, mt * scale_log2);
     // lazy rescale: only when the running max grows by more than 2^8
     const bool rescale = m_new > m + 8.f;
@@ -143,23 +159,25 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
       m = m_new;
     }
     const float mb = (m == -INFINITY) ? 0.f : m;
+    const float2 sc2 = make_float2(scale_log2, scale_log2), nmb2 = make_float2(-mb, -mb);
+    float2 ls = make_float2(0.f, 0.f);  // one chain: its FADD2 latency hides under MUFU
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float x0 = fmaf(s[c * 32 + 2 * i], scale_log2, -mb);
-        const float x1 = fmaf(s[c * 32 + 2 * i + 1], scale_log2, -mb);
-        // a share of the exponentials runs on the FMA pipe so MUFU is not the
-        // softmax bottleneck (every kPolyEvery-th pair's second element)
-        const float p0 = ex2(x0);
-        const float p1 = (kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) ? ex2_poly(x1)
-                                                                                 : ex2(x1);
-        l += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
+        const float2 x = ffma2(make_float2(__uint_as_float(sr[c * 32 + 2 * i]),
+                                           __uint_as_float(sr[c * 32 + 2 * i + 1])),
+                               sc2, nmb2);
+        const float2 pp = (kPolyEvery > 0 && (c * 16 + i) % kPolyEvery == kPolyEvery - 1)
+                              ? ex2_poly2(x)
+                              : make_float2(ex2(x.x), ex2(x.y));
+        ls = fadd2(ls, pp);
+        pk[i] = pack_bf16(pp.x, pp.y);
       }
       BAM_TMEM_ST16(tmem + lane_base + colS + c * 16, pk);
     }
+    l += ls.x + ls.y;
     // warp-uniform branch: tcgen05.ld/st are .sync.aligned (alpha == 1 for rows that keep m).
     // O(t-1) is complete: S(t) was issued after PV(t-1) and its commit covers it.
     if (__any_sync(0xffffffffu, rescale) && t > 0) {
@@ -325,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   } else {
     // ------------------------------------------------------------ softmax warps 0-3
-    softmax_role(p, tmem, kColS, kColO, &sm.bar_s_full, &sm.bar_p_full, &sm.bar_pv_done, j, h,
+    softmax_role<BAM_FWD_POLY_MHA>(p, tmem, kColS, kColO, &sm.bar_s_full, &sm.bar_p_full, &sm.bar_pv_done, j, h,
                  warp, lane, tiles, n, slot);
   }
   tc_fence_before();
@@ -476,7 +494,7 @@ __global__ void __maxnreg__(168)
   } else {
     // ------------------------------------------------------------ softmax warpgroups
     const int i = warp >> 2;  // tile 0: warps 0-3, tile 1: warps 4-7
-    softmax_role(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i], &sm.bar_p_ready[i],
+    softmax_role<BAM_FWD_POLY_PAIR>(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i], &sm.bar_p_ready[i],
                  &sm.bar_pv_done[i], j, h0 + i, warp, lane, tiles, n, slot);
   }
   tc_fence_before();
