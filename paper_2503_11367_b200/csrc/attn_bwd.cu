@@ -56,6 +56,15 @@ constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
 #define BAM_BWD_KVT 0
 #endif
 constexpr int kStages = (BAM_DQ_BULK && !BAM_BWD_KVT) ? 3 : 4;
+// Grid order.  Slot-major (key blocks fastest, one KV head after the other):
+// the ~148 CTAs resident together are key blocks of ONE KV head, so their dQ
+// reductions land in that head group's quarter-GiB slice of dq_acc, whose
+// active window stays in L2.  Head-major (KV heads fastest) spreads each wave
+// over all eight slices and re-reads dq_acc from DRAM once per wave.
+#ifndef BAM_BWD_SLOT_MAJOR
+#define BAM_BWD_SLOT_MAJOR 1
+#endif
+constexpr bool kSlotMajor = BAM_BWD_SLOT_MAJOR;
 constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
 constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
 constexpr uint32_t kDsBytes = 128 * 64 * 2;      // dS^T: 128 key rows x 64 query cols
@@ -161,10 +170,10 @@ __global__ void __maxnreg__(128)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int hkv = blockIdx.x;
+  const int hkv = kSlotMajor ? blockIdx.y : blockIdx.x;
   // CTA-pair mode: clusters of 2 along y; slot lists; shared pairs multicast Q/dO
   const bool cluster_mode = p.pair_shared != nullptr;
-  const int slot = blockIdx.y;
+  const int slot = kSlotMajor ? blockIdx.x : blockIdx.y;
   const int kb = p.order ? p.order[slot] : slot;   // -1: padding slot (cluster mode)
   const int li = cluster_mode ? slot : kb;         // step-list index
   const uint32_t crank = cluster_mode ? cluster_ctarank() : 0;
@@ -843,20 +852,20 @@ int bam_attn_bwd_main(const BamAttnBwdParams* pp, void* stream) {
     BAM_CHECK_ARG(p.n_slots >= 2 && p.n_slots % 2 == 0 && p.order != nullptr,
                   "bam_attn_bwd: pair mode needs an even n_slots=%d and slot_kb", p.n_slots);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.Hkv, p.n_slots);
+    cfg.gridDim = bwd::kSlotMajor ? dim3(p.n_slots, p.Hkv) : dim3(p.Hkv, p.n_slots);
     cfg.blockDim = dim3(bwd::kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 2;
+    attr[0].val.clusterDim.x = bwd::kSlotMajor ? 2 : 1;
+    attr[0].val.clusterDim.y = bwd::kSlotMajor ? 1 : 2;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     BAM_CUDA_TRY(cudaLaunchKernelEx(&cfg, bwd::attn_bwd_kernel, mq, mk, mv, mdo, p));
   } else {
-    dim3 grid(p.Hkv, p.nb);
+    const dim3 grid = bwd::kSlotMajor ? dim3(p.nb, p.Hkv) : dim3(p.Hkv, p.nb);
     bwd::attn_bwd_kernel<<<grid, bwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, mdo, p);
   }
   BAM_LAUNCH_CHECK();

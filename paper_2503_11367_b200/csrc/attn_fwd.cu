@@ -102,6 +102,14 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // owns row r = 32 w + lane = TMEM lane r.  Per key tile t: wait S(t), mask
 // PARTIAL tiles, online softmax (log2 domain, lazy 2^8 rescale of O in TMEM),
 // P -> bf16 into the S columns, arrive p_ready.  Finally O / l -> bf16, LSE.
+// Grid order.  Row-major (query blocks / work items fastest, heads slowest):
+// the CTAs resident together read the K/V tiles of one KV head, which stay in
+// L2; head-major spreads every wave over all KV heads.
+#ifndef BAM_FWD_ROW_MAJOR
+#define BAM_FWD_ROW_MAJOR 1
+#endif
+constexpr bool kRowMajor = BAM_FWD_ROW_MAJOR;
+
 template <int kPolyEvery>
 __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t tmem,
                                              uint32_t colS, uint32_t colO, uint64_t* bar_s_full,
@@ -259,8 +267,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                                       ~uintptr_t(1023));
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
-  const int h = p.h_begin + blockIdx.x;
-  const WorkItem wi = work_item(p, blockIdx.y);
+  const int h = p.h_begin + (kRowMajor ? blockIdx.y : blockIdx.x);
+  const WorkItem wi = work_item(p, kRowMajor ? blockIdx.x : blockIdx.y);
   const int j = wi.j, n = wi.n, slot = wi.slot;
   const int32_t* tiles = wi.tiles;
   const int hkv = (h - p.h_begin) / (nh / p.Hkv);
@@ -381,8 +389,8 @@ __global__ void __maxnreg__(168)
   PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
-  const int h0 = p.h_begin + 2 * blockIdx.x;
-  const WorkItem wi = work_item(p, blockIdx.y);
+  const int h0 = p.h_begin + 2 * (kRowMajor ? blockIdx.y : blockIdx.x);
+  const WorkItem wi = work_item(p, kRowMajor ? blockIdx.x : blockIdx.y);
   const int j = wi.j, n = wi.n, slot = wi.slot;
   const int32_t* tiles = wi.tiles;
   const int hkv = (h0 - p.h_begin) / (nh / p.Hkv);
@@ -589,14 +597,16 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
     const int smem = (int)sizeof(fwd::PairSmem);
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_pair_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid(nh / 2, p.items ? p.n_items : p.nq);
+    const int rows = p.items ? p.n_items : p.nq;
+    const dim3 grid = fwd::kRowMajor ? dim3(rows, nh / 2) : dim3(nh / 2, rows);
     fwd::attn_fwd_pair_kernel<<<grid, fwd::kPairThreads, smem, (cudaStream_t)stream>>>(mq, mk,
                                                                                        mv, p);
   } else {
     const int smem = (int)sizeof(fwd::Smem) + 1024;
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    dim3 grid(nh, p.items ? p.n_items : p.nq);
+    const int rows = p.items ? p.n_items : p.nq;
+    const dim3 grid = fwd::kRowMajor ? dim3(rows, nh) : dim3(nh, rows);
     fwd::attn_fwd_kernel<<<grid, fwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, p);
   }
   BAM_LAUNCH_CHECK();
