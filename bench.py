@@ -63,8 +63,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=2)
-    ap.add_argument("--groups", type=int, default=2,
-                    help="KV-head groups pipelining the CP collectives with compute (N > 1)")
+    ap.add_argument("--groups", type=int, default=1,
+                    help="KV-head groups pipelining the CP collectives with compute (N > 1); "
+                         "1 measured best at N=2/4 (profiles/r01/head_group_ablation.md)")
     return ap.parse_args()
 
 

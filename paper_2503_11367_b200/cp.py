@@ -196,7 +196,7 @@ def _head_groups(Hkv: int, groups: int):
     return [(g * per, per) for g in range(groups)]
 
 
-def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups: int = 2):
+def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups: int = 1):
     """All-gather K/V per KV-head group on a side stream; the forward of group
     g starts as soon as its K/V have landed, overlapping the gather of group
     g+1 (the paper overlaps communication per head).
@@ -276,7 +276,7 @@ class _CPAttention(torch.autograd.Function):
 
 
 def cp_bitfield_attention(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None,
-                          groups: int = 2):
+                          groups: int = 1):
     """Context-parallel bitfield attention with autograd.  Inputs are this
     rank's rows (``shard_rows``) of q/k/v; returns this rank's O rows.  K/V
     travel in ``groups`` KV-head groups so communication overlaps compute."""
