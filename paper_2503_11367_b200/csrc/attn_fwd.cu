@@ -177,7 +177,8 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
         const float2 x = ffma2(make_float2(__uint_as_float(sr[c * 32 + 2 * i]),
                                            __uint_as_float(sr[c * 32 + 2 * i + 1])),
                                sc2, nmb2);
-        const float2 pp = (kPolyEvery > 0 && (c * 16 + i) % kPolyEvery == kPolyEvery - 1)
+        const float2 pp = (kPolyEvery > 0 && (c * 16 + i) % (kPolyEvery > 0 ? kPolyEvery : 1) ==
+                                                 kPolyEvery - 1)
                               ? ex2_poly2(x)
                               : make_float2(ex2(x.x), ex2(x.y));
         ls = fadd2(ls, pp);
@@ -370,6 +371,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 // tile's MMAs:  S0(0) S1(0) | PV0(0) S0(1) | PV1(0) S1(1) | PV0(1) S0(2) | ...
 // K/V tiles stream through a 2-stage ring.
 //   warps 0-3 softmax tile 0, warps 4-7 softmax tile 1, warp 8 TMA, warp 9 MMA.
+// 168 registers is the ceiling at 320 threads (registers are allocated for
+// whole warpgroups: 12 x 32 x 168 = 64512; 176 fails to launch); the softmax
+// then spills a few loop invariants (~60 B / thread).
 constexpr int kPairThreads = 320;
 
 struct PairSmem {
