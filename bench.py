@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=2)
+    ap.add_argument("--transport", default="ce", choices=["nccl", "ce"],
+                    help="CP exchange: NCCL collectives or copy-engine pulls/pushes over "
+                         "symmetric memory (N > 1)")
     ap.add_argument("--groups", type=int, default=1,
                     help="KV-head groups pipelining the CP collectives with compute (N > 1); "
                          "1 measured best at N=2/4 (profiles/r01/head_group_ablation.md)")
@@ -229,15 +232,23 @@ def main():
     flop_local_bwd = 10.0 * D * Hq * n_allowed / world
 
     n_groups = args.groups if world > 1 else 1
+    if world > 1 and args.transport == "ce":
+        try:   # symmetric-memory rendezvous; NCCL collectives if the box cannot map peers
+            plan.exchange(CP._head_groups(Hkv, n_groups), D, dev)
+        except Exception as exc:  # noqa: BLE001
+            print(f"bench: copy-engine transport unavailable ({exc}); using NCCL", file=sys.stderr)
+            args.transport = "nccl"
 
     def step(ev):
         """ev: [fwd start, fwd end, bwd end, (main start, main end) per head group...]"""
         if world > 1:
             ev[0].record()
-            o, lse, gathered = CP.cp_forward(q_loc, k_loc, v_loc, plan, groups=n_groups)
+            o, lse, gathered = CP.cp_forward(q_loc, k_loc, v_loc, plan, groups=n_groups,
+                                             transport=args.transport)
             ev[1].record()
             timers = [(ev[3 + 2 * i], ev[4 + 2 * i]) for i in range(len(gathered))]
-            dq, dk, dv = CP.cp_backward(q_loc, gathered, o, lse, do_loc, plan, timers=timers)
+            dq, dk, dv = CP.cp_backward(q_loc, gathered, o, lse, do_loc, plan, timers=timers,
+                                        transport=args.transport)
             ev[2].record()
             return dq, dk, dv
         ev[0].record()
@@ -326,7 +337,8 @@ def main():
             qd, kd, vd = (t.detach().requires_grad_(True) for t in dev_in[b][:3])
             dod = dev_in[b][3]
             if world > 1:
-                o = CP.cp_bitfield_attention(qd, kd, vd, plan, groups=n_groups)
+                o = CP.cp_bitfield_attention(qd, kd, vd, plan, groups=n_groups,
+                                             transport=args.transport)
             else:
                 o = A.bitfield_attention(qd, kd, vd, plan.attn)
             o.backward(dod)
@@ -389,6 +401,7 @@ def main():
             "config": {"workload": cfg["name"], "tokens": T, "Hq": Hq, "Hkv": Hkv, "head_dim": D,
                        "cp": world, "policy": args.policy, "n_allowed": n_allowed,
                        "kv_head_groups": n_groups,
+                       "transport": args.transport if world > 1 else None,
                        "flop_per_step": flop_step,
                        "l2": "inputs larger than L2 (Q alone %.2f GiB per rank)" %
                              (q_loc.numel() * 2 / 2**30)},

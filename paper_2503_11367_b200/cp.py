@@ -149,12 +149,87 @@ def scatter_dkv(dk_all: torch.Tensor, dv_all: torch.Tensor, layout: CPLayout, gr
     return dk[:n], dv[:n]
 
 
+class SymmExchange:
+    """Copy-engine K/V all-gather and dK/dV reduce-scatter over NVLink peer
+    memory (torch symmetric memory, CUDA IPC).  Every rank's
+    K/V shard lives in a symmetric buffer that the peers PULL with
+    cudaMemcpyAsync, and the dK/dV partials are PUSHED into the owners'
+    symmetric workspaces, so the transfers run on the copy engines and take
+    no SMs from the attention kernels (NCCL's kernels do).  Per KV-head group
+    the buffers are contiguous, so one copy moves one rank's group slice."""
+
+    def __init__(self, layout: CPLayout, head_groups, d: int, device, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        pg = group if group is not None else dist.group.WORLD
+        self.world, self.rank = layout.world, layout.rank
+        self.rows, self.d, self.n_local = layout.max_blocks * BLOCK, d, layout.n_local * BLOCK
+        self.kv_off, self.ws_off = [], []
+        kv_n = ws_n = 0
+        for _, nkv in head_groups:
+            per = self.rows * nkv * d
+            self.kv_off.append(kv_n)
+            self.ws_off.append(ws_n)
+            kv_n += 2 * per
+            ws_n += self.world * 2 * per
+        self.kv = symm_mem.empty((kv_n,), dtype=torch.bfloat16, device=device)
+        self.kv_h = symm_mem.rendezvous(self.kv, pg.group_name)
+        self.ws = symm_mem.empty((ws_n,), dtype=torch.float32, device=device)
+        self.ws_h = symm_mem.rendezvous(self.ws, pg.group_name)
+
+    def gather(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor):
+        """This rank's [n_local*128, nkv, d] K/V slice of head group gi ->
+        gathered rank-major [world*rows, nkv, d] K and V (the NCCL layout)."""
+        nkv, rows, d = k_g.shape[1], self.rows, self.d
+        per = rows * nkv * d
+        mine = self.kv[self.kv_off[gi]:self.kv_off[gi] + 2 * per].view(2, rows, nkv, d)
+        mine[0, :k_g.shape[0]].copy_(k_g)
+        mine[1, :v_g.shape[0]].copy_(v_g)
+        k_all = torch.empty((self.world * rows, nkv, d), dtype=k_g.dtype, device=k_g.device)
+        v_all = torch.empty_like(k_all)
+        self.kv_h.barrier(channel=0)          # every rank's slice is in place
+        for step in range(self.world):
+            r = (self.rank + step) % self.world
+            src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, self.kv_off[gi])
+            k_all[r * rows:(r + 1) * rows].copy_(src[0])
+            v_all[r * rows:(r + 1) * rows].copy_(src[1])
+        self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
+        return k_all, v_all
+
+    def reduce_scatter(self, gi: int, dk_all: torch.Tensor, dv_all: torch.Tensor):
+        """fp32 partials [world*rows, nkv, d] of every key -> this rank's
+        summed [n_local*128, nkv, d] dK and dV."""
+        nkv, rows, d = dk_all.shape[1], self.rows, self.d
+        per = rows * nkv * d
+        base = self.ws_off[gi]
+        for step in range(self.world):
+            r = (self.rank + step) % self.world
+            dst = self.ws_h.get_buffer(r, (2, rows, nkv, d), torch.float32,
+                                       base + self.rank * 2 * per)
+            dst[0].copy_(dk_all[r * rows:(r + 1) * rows])
+            dst[1].copy_(dv_all[r * rows:(r + 1) * rows])
+        self.ws_h.barrier(channel=0)          # every rank's partials have landed
+        red = self.ws[base:base + self.world * 2 * per].view(self.world, 2, rows, nkv, d).sum(0)
+        self.ws_h.barrier(channel=0)          # summed before the next pushes
+        return red[0, :self.n_local], red[1, :self.n_local]
+
+
 @dataclass
 class CPPlan:
     layout: CPLayout
     attn: A.AttentionPlan
     assignment: B.DeviceAssignment
     policy: str
+    _exchange: dict = None
+
+    def exchange(self, head_groups, d, device, group=None) -> SymmExchange:
+        """The copy-engine transport for this plan (built once per head-group split)."""
+        key = (tuple(head_groups), d, str(device), id(group))
+        if self._exchange is None:
+            self._exchange = {}
+        if key not in self._exchange:
+            self._exchange[key] = SymmExchange(self.layout, head_groups, d, device, group)
+        return self._exchange[key]
 
     @property
     def predicted_imbalance(self) -> float:
@@ -196,11 +271,18 @@ def _head_groups(Hkv: int, groups: int):
     return [(g * per, per) for g in range(groups)]
 
 
-def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups: int = 1):
+TRANSPORTS = ("nccl", "ce")
+
+
+def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups: int = 1,
+               transport: str = "nccl"):
     """All-gather K/V per KV-head group on a side stream; the forward of group
     g starts as soon as its K/V have landed, overlapping the gather of group
     g+1 (the paper overlaps communication per head).
-    Returns (o, lse, [(k_all_g, v_all_g)])."""
+    transport "nccl": NCCL all_gather; "ce": copy-engine pulls from symmetric
+    memory (SymmExchange).  Returns (o, lse, [(k_all_g, v_all_g)])."""
+    if transport not in TRANSPORTS:
+        raise ValueError(f"transport must be one of {TRANSPORTS}")
     Hq, Hkv = q_loc.shape[1], k_loc.shape[1]
     grp = Hq // Hkv
     cur = torch.cuda.current_stream()
@@ -208,12 +290,17 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     o = torch.empty_like(q_loc)
     lse = torch.empty(Hq, q_loc.shape[0], dtype=torch.float32, device=q_loc.device)
     gathered, events = [], []
+    hg = _head_groups(Hkv, groups)
+    ex = plan.exchange(hg, k_loc.shape[2], k_loc.device, group) if transport == "ce" else None
     comm.wait_stream(cur)
     with torch.cuda.stream(comm):
-        for kv0, nkv in _head_groups(Hkv, groups):
-            kg = k_loc[:, kv0:kv0 + nkv].contiguous()
-            vg = v_loc[:, kv0:kv0 + nkv].contiguous()
-            k_all, v_all = gather_kv(kg, vg, plan.layout, group)
+        for gi, (kv0, nkv) in enumerate(hg):
+            if ex is not None:
+                k_all, v_all = ex.gather(gi, k_loc[:, kv0:kv0 + nkv], v_loc[:, kv0:kv0 + nkv])
+            else:
+                kg = k_loc[:, kv0:kv0 + nkv].contiguous()
+                vg = v_loc[:, kv0:kv0 + nkv].contiguous()
+                k_all, v_all = gather_kv(kg, vg, plan.layout, group)
             ev = torch.cuda.Event()
             ev.record(comm)
             gathered.append((k_all, v_all))
@@ -228,7 +315,7 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
 
 
 def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=None,
-                timers=None):
+                timers=None, transport: str = "nccl"):
     """Per KV-head group: backward kernel -> fp32 dK/dV partials of every key,
     reduce-scattered on the side stream while the next group computes."""
     Hq = q_loc.shape[1]
@@ -237,6 +324,9 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
     cur = torch.cuda.current_stream()
     comm = _comm_stream(q_loc.device)
     ws = A.BackwardWorkspace(q_loc, o, lse, do, plan.attn, scale)
+    hg = [(sum(k.shape[1] for k, _ in gathered[:i]), k.shape[1]) for i, (k, _) in
+          enumerate(gathered)]
+    ex = plan.exchange(hg, q_loc.shape[2], q_loc.device, group) if transport == "ce" else None
     parts, kv0 = [], 0
     for i, (k_all, v_all) in enumerate(gathered):
         nkv = k_all.shape[1]
@@ -248,7 +338,8 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
             comm.wait_event(ev)
             dk_all.record_stream(comm)
             dv_all.record_stream(comm)
-            parts.append(scatter_dkv(dk_all, dv_all, plan.layout, group))
+            parts.append(ex.reduce_scatter(i, dk_all, dv_all) if ex is not None else
+                         scatter_dkv(dk_all, dv_all, plan.layout, group))
         kv0 += nkv
     dq = ws.finalize()
     cur.wait_stream(comm)
@@ -259,11 +350,11 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
 
 class _CPAttention(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, plan, group, scale, groups):
-        o, lse, gathered = cp_forward(q, k, v, plan, group, scale, groups)
+    def forward(ctx, q, k, v, plan, group, scale, groups, transport):
+        o, lse, gathered = cp_forward(q, k, v, plan, group, scale, groups, transport)
         flat = [t for kv in gathered for t in kv]
         ctx.save_for_backward(q, o, lse, *flat)
-        ctx.plan, ctx.group, ctx.scale = plan, group, scale
+        ctx.plan, ctx.group, ctx.scale, ctx.transport = plan, group, scale, transport
         return o
 
     @staticmethod
@@ -271,13 +362,14 @@ class _CPAttention(torch.autograd.Function):
         q, o, lse, *flat = ctx.saved_tensors
         gathered = list(zip(flat[0::2], flat[1::2]))
         dq, dk, dv = cp_backward(q, gathered, o, lse, do.contiguous(), ctx.plan, ctx.group,
-                                 ctx.scale)
-        return dq, dk, dv, None, None, None, None
+                                 ctx.scale, transport=ctx.transport)
+        return dq, dk, dv, None, None, None, None, None
 
 
 def cp_bitfield_attention(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None,
-                          groups: int = 1):
+                          groups: int = 1, transport: str = "nccl"):
     """Context-parallel bitfield attention with autograd.  Inputs are this
     rank's rows (``shard_rows``) of q/k/v; returns this rank's O rows.  K/V
-    travel in ``groups`` KV-head groups so communication overlaps compute."""
-    return _CPAttention.apply(q_loc, k_loc, v_loc, plan, group, scale, groups)
+    travel in ``groups`` KV-head groups so communication overlaps compute,
+    over NCCL (``transport="nccl"``) or the copy engines (``"ce"``)."""
+    return _CPAttention.apply(q_loc, k_loc, v_loc, plan, group, scale, groups, transport)

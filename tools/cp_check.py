@@ -23,6 +23,8 @@ from paper_2503_11367_b200 import cp, mask as M  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--policy", default="lpt")
+ap.add_argument("--transport", default="nccl", choices=["nccl", "ce"])
+ap.add_argument("--groups", type=int, default=1)
 args = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 local = int(os.environ.get("LOCAL_RANK", rank))
@@ -44,8 +46,12 @@ q_loc, k_loc, v_loc, do_loc = cp.shard_rows(*(t.to(dev) for t in (q, k, v, do)),
 q_loc.requires_grad_(True)
 k_loc.requires_grad_(True)
 v_loc.requires_grad_(True)
-o = cp.cp_bitfield_attention(q_loc, k_loc, v_loc, plan)
-o.backward(do_loc)
+for _ in range(2):   # twice: the second step reuses the transport's buffers
+    for t in (q_loc, k_loc, v_loc):
+        t.grad = None
+    o = cp.cp_bitfield_attention(q_loc, k_loc, v_loc, plan, groups=args.groups,
+                                 transport=args.transport)
+    o.backward(do_loc)
 torch.cuda.synchronize()
 
 # gather every rank's rows (padded to max_blocks) on rank 0
@@ -77,7 +83,8 @@ if rank == 0:
         rl = ((full - refs[name]).norm() / refs[name].norm()).item()
         report[name] = {"max_abs": ma, "rel_l2": rl, "ok": ma <= 2e-2 and rl <= 1e-2}
     ok = all(x["ok"] for x in report.values())
-    print(json.dumps({"world": world, "policy": args.policy, "ok": ok,
+    print(json.dumps({"world": world, "policy": args.policy, "transport": args.transport,
+                      "groups": args.groups, "ok": ok,
                       "imbalance_predicted": plan.predicted_imbalance, **report}))
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
