@@ -150,3 +150,42 @@ def test_permute_blocks_gather_scatter_bit_exact():
     bad = torch.zeros(T, 3, device=dev, dtype=torch.bfloat16)   # 6-B rows
     with pytest.raises(_lib.BamError, match="16-byte"):
         cp.shard_rows(bad, lay)
+
+
+@pytest.mark.parametrize("transport", ["nccl", "ce"])
+def test_cp_single_rank_transports_match_local(transport):
+    """cp_bitfield_attention on a one-rank NCCL process group, through both
+    exchange transports (NCCL collectives; copy-engine pulls/pushes over
+    symmetric memory): equal to the single-GPU autograd path."""
+    import torch.distributed as dist
+
+    from paper_2503_11367_b200 import attention as A
+    from paper_2503_11367_b200 import cp
+    from paper_2503_11367_b200 import mask as M
+
+    if not dist.is_initialized():
+        import socket
+        with socket.socket() as sck:
+            sck.bind(("127.0.0.1", 0))
+            port = sck.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                world_size=1, device_id=torch.device("cuda", 0))
+    mask = M.build_bitfield([("text", 256), ("img0", 384), ("text", 512), ("img1", 128)])
+    T, Hq, Hkv = len(mask), 8, 4
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(3)
+    q, k, v, do = (torch.randn(T, h, 128, device=dev, generator=g).to(torch.bfloat16)
+                   for h in (Hq, Hkv, Hkv, Hq))
+    plan = cp.make_cp_plan(mask, 1, 0, "lpt")
+    outs = []
+    for fn in ("local", transport):
+        qd, kd, vd = (t.clone().requires_grad_(True) for t in (q, k, v))
+        if fn == "local":
+            o = A.bitfield_attention(qd, kd, vd, plan.attn)
+        else:
+            o = cp.cp_bitfield_attention(qd, kd, vd, plan, groups=2, transport=transport)
+        o.backward(do)
+        outs.append((o.detach(), qd.grad, kd.grad, vd.grad))
+    for name, a, b in zip(("O", "dQ", "dK", "dV"), *outs):
+        assert (a.float() - b.float()).abs().max().item() < 1e-2, name
+    assert torch.equal(outs[0][0], outs[1][0])
