@@ -62,6 +62,16 @@ def cmd_cp_distribute(args: argparse.Namespace) -> int:
             "makespan": optimal.makespan,
             "imbalance": optimal.imbalance,
         }
+    if args.measure:
+        # measured makespans on this B200 (8(f)3); absent from the default,
+        # byte-identical report
+        from . import measure
+        doc["measured"] = {
+            "heads": args.heads, "kv_heads": args.kv_heads, "head_dim": 128,
+            "unit": "ms of fwd+bwd kernels per rank (ranks emulated on one GPU)",
+            "policies": measure.measure_policies(mask, args.gpus, args.subblock_size,
+                                                 heads=args.heads, kv_heads=args.kv_heads),
+        }
     _write_json(doc, args.output)
     return EXIT_OK
 
@@ -84,6 +94,11 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--ilp", action="store_true",
                    help="also solve the exact assignment (small instances only)")
     p.add_argument("--output", "-o", default=None, help="report path (default stdout)")
+    p.add_argument("--measure", action="store_true",
+                   help="also run every rank's attention fwd+bwd per policy on this GPU and "
+                        "report measured makespans (adds a 'measured' key)")
+    p.add_argument("--heads", type=int, default=32, help="query heads for --measure")
+    p.add_argument("--kv-heads", type=int, default=8, help="KV heads for --measure")
     p.set_defaults(func=cmd_cp_distribute)
     return parser
 
