@@ -140,6 +140,39 @@ constexpr bool kMmaOnly = true;
 constexpr bool kMmaOnly = false;
 #endif
 
+// P = 2^(S c - lse) for a pair of queries (packed FFMA2), one in kBwdPoly
+// pairs on the FMA pipe (ex2_poly2), masked by the PARTIAL-tile allow bits.
+#ifndef BAM_BWD_POLY_EVERY
+#define BAM_BWD_POLY_EVERY 0
+#endif
+constexpr int kBwdPoly = BAM_BWD_POLY_EVERY;
+// (The all-SS kernel runs at 128 registers and keeps the scalar forms: the
+// register pairs FFMA2 needs make it spill; its softmax is off the MMA chain.)
+__device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, const float4& v, float sc,
+                                         int i2, uint32_t allow) {
+#if BAM_BWD_KVT
+  const float2 x = ffma2(make_float2(__uint_as_float(s0), __uint_as_float(s1)),
+                         make_float2(sc, sc), make_float2(-v.x, -v.z));
+#else
+  const float2 x = make_float2(fmaf(__uint_as_float(s0), sc, -v.x), fmaf(__uint_as_float(s1), sc, -v.z));
+#endif
+  float2 p = (kBwdPoly > 0 && i2 % (kBwdPoly > 0 ? kBwdPoly : 1) == kBwdPoly - 1)
+                 ? ex2_poly2(x)
+                 : make_float2(ex2(x.x), ex2(x.y));
+  p.x = (allow >> (2 * i2)) & 1 ? p.x : 0.f;
+  p.y = (allow >> (2 * i2 + 1)) & 1 ? p.y : 0.f;
+  return p;
+}
+// dS = P (dP - D) for the same pair
+__device__ __forceinline__ float2 ds_pair(float2 p, uint32_t dp0, uint32_t dp1, const float4& v) {
+#if BAM_BWD_KVT
+  return fmul2(p, fadd2(make_float2(__uint_as_float(dp0), __uint_as_float(dp1)),
+                        make_float2(-v.y, -v.w)));
+#else
+  return make_float2(p.x * (__uint_as_float(dp0) - v.y), p.y * (__uint_as_float(dp1) - v.w));
+#endif
+}
+
 struct StepInfo {
   int h, jq, cls, half;
 };
@@ -480,14 +513,10 @@ __global__ void __maxnreg__(128)
         uint32_t pk[16];
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
-          const float4 v = ld[i2];
-          float p0 = ex2(fmaf(__uint_as_float(sr[2 * i2]), scale_log2, -v.x));
-          float p1 = ex2(fmaf(__uint_as_float(sr[2 * i2 + 1]), scale_log2, -v.z));
-          p0 = (allow >> (2 * i2)) & 1 ? p0 : 0.f;
-          p1 = (allow >> (2 * i2 + 1)) & 1 ? p1 : 0.f;
-          sr[2 * i2] = __float_as_uint(p0);
-          sr[2 * i2 + 1] = __float_as_uint(p1);
-          pk[i2] = pack_bf16(p0, p1);
+          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], ld[i2], scale_log2, i2, allow);
+          sr[2 * i2] = __float_as_uint(pp.x);
+          sr[2 * i2 + 1] = __float_as_uint(pp.y);
+          pk[i2] = pack_bf16(pp.x, pp.y);
         }
         BAM_TMEM_ST16(tS + c * 32, pk);  // P^T over this warpgroup's own S columns
       }
@@ -503,9 +532,10 @@ __global__ void __maxnreg__(128)
       tmem_wait_ld();
 #pragma unroll
       for (int i2 = 0; i2 < 16; ++i2) {
-        const float4 v = ld[i2];
-        dsk[i2] = pack_bf16(__uint_as_float(sr[2 * i2]) * (__uint_as_float(dr[2 * i2]) - v.y),
-                            __uint_as_float(sr[2 * i2 + 1]) * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
+        const float2 ds = ds_pair(make_float2(__uint_as_float(sr[2 * i2]),
+                                              __uint_as_float(sr[2 * i2 + 1])),
+                                  dr[2 * i2], dr[2 * i2 + 1], ld[i2]);
+        dsk[i2] = pack_bf16(ds.x, ds.y);
       }
       // dS^T row r, query columns 32c .. 32c+31 (the A operand of dK, B of dQ^T)
 #pragma unroll
@@ -550,13 +580,10 @@ __global__ void __maxnreg__(128)
 #pragma unroll
       for (int i2 = 0; i2 < 16; ++i2) {
         const float4 v = ld[i2];
-        float p0 = ex2(fmaf(__uint_as_float(sr[2 * i2]), scale_log2, -v.x));
-        float p1 = ex2(fmaf(__uint_as_float(sr[2 * i2 + 1]), scale_log2, -v.z));
-        p0 = (allow >> (2 * i2)) & 1 ? p0 : 0.f;
-        p1 = (allow >> (2 * i2 + 1)) & 1 ? p1 : 0.f;
-        pk[i2] = pack_bf16(p0, p1);
-        dsk[i2] = pack_bf16(p0 * (__uint_as_float(dr[2 * i2]) - v.y),
-                            p1 * (__uint_as_float(dr[2 * i2 + 1]) - v.w));
+        const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], v, scale_log2, i2, allow);
+        const float2 ds = ds_pair(pp, dr[2 * i2], dr[2 * i2 + 1], v);
+        pk[i2] = pack_bf16(pp.x, pp.y);
+        dsk[i2] = pack_bf16(ds.x, ds.y);
       }
       BAM_TRACE_EV(threadIdx.x == 0, 18, s);
       // P^T (bf16 pairs) goes over the S columns this warpgroup itself read,

@@ -420,6 +420,35 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (packed FFMA2): x = n + f, f in [-0.5, 0.5]
+// (round via the 1.5*2^23 magic constant), 2^f by a degree-4 polynomial
+// (rel. err < 4e-6, well below bf16 P rounding), exponent n added to the
+// float bits.  x <= 8 (the forward's lazy rescale; x <= 0 in the backward); clamping at -127 makes 2^x flush
+// to ~0 like ex2.approx.ftz.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.f;
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));  // integer part in the low bits
+  const float2 f = ffma2(fadd2(t, make_float2(-kMagic, -kMagic)), make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(1.3333558e-3f, 1.3333558e-3f), f,
+                   make_float2(9.6181291e-3f, 9.6181291e-3f));
+  p = ffma2(p, f, make_float2(5.5504109e-2f, 5.5504109e-2f));
+  p = ffma2(p, f, make_float2(2.4022651e-1f, 2.4022651e-1f));
+  p = ffma2(p, f, make_float2(6.9314718e-1f, 6.9314718e-1f));
+  p = ffma2(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
