@@ -217,6 +217,18 @@ int bam_build_pair_lists(const int32_t* col_off, const int32_t* col_tiles, const
                          int32_t nb, int32_t* slot_kb, int32_t* slot_cnt, int32_t* slot_off,
                          int32_t* slot_tiles, int32_t* pair_shared, void* stream);
 
+/* Forward on CTA pairs (tcgen05 cta_group::2, M = 256): for every shared pair
+ * pr = pair_ids[i] of bam_build_pair_lists run over the ROW lists (row_off /
+ * row_tiles, order = heavy-first query blocks), the two query blocks
+ * slot_q[2 pr], slot_q[2 pr + 1] walk their common union list
+ * slot_tiles[slot_off[s] .. slot_off[s + 1]) with the K/V operand traffic
+ * split across the two SMs.  Needs an even GQA group (nh / Hkv); whole rows
+ * only (p->items unused).  Query blocks of non-shared pairs go through
+ * bam_attn_fwd with a whole-row items list. */
+int bam_attn_fwd_2cta(const BamAttnFwdParams* p, const int32_t* pair_ids, int32_t n_pairs,
+                      const int32_t* slot_q, const int32_t* slot_off, const int32_t* slot_tiles,
+                      void* stream);
+
 /* ---- token permutation ----------------- */
 /* The CP runtime permutes tokens into the LPT block layout before attention
  * and back afterwards.  Block-row gather / scatter for up to BAM_PERMUTE_MAX

@@ -70,6 +70,8 @@ SIGNATURES = {
     "bam_attn_bwd_finalize": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "bam_permute_blocks": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "bam_attn_fwd_2cta": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp, c_i32, c_vp, c_vp, c_vp,
+                                  c_vp]),
     "bam_build_pair_lists": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bam_selftest_umma": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bam_set_trace_buffer": (c_i32, [c_vp]),

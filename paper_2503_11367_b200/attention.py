@@ -51,6 +51,13 @@ class AttentionPlan:
     slot_off: torch.Tensor | None = None
     slot_tiles: torch.Tensor | None = None
     pair_shared: torch.Tensor | None = None
+    # forward CTA pairs (cta_group::2): shared pairs of heavy-first query blocks
+    # and a whole-row items list (j, 0, W, -1) for the blocks of the other pairs
+    fwd_pair_ids: torch.Tensor | None = None
+    fwd_slot_q: torch.Tensor | None = None
+    fwd_slot_off: torch.Tensor | None = None
+    fwd_slot_tiles: torch.Tensor | None = None
+    fwd_rest_items: torch.Tensor | None = None
 
     @property
     def nq(self) -> int:
@@ -108,11 +115,39 @@ def build_plan(desc: torch.Tensor, q_gid: torch.Tensor | None = None,
     _lib.call("bam_build_pair_lists", col_off.data_ptr(), col_tiles.data_ptr(),
               bwd_order.data_ptr(), nb, slot_kb.data_ptr(), slot_cnt.data_ptr(),
               slot_off.data_ptr(), slot_tiles.data_ptr(), pair_shared.data_ptr())
+    fwd_order = _heavy_first(row_cnt)
+    fp = _fwd_pairs(row_off, row_tiles, row_cnt, fwd_order, nq, dev)
     return AttentionPlan(desc=desc, nb=nb, classes=classes, W=W, q_gid=q_gid.to(torch.int32),
                          k_row=k_row.to(torch.int32), k_rows=int(k_rows), row_off=row_off,
                          row_tiles=row_tiles, col_off=col_off, col_tiles=col_tiles,
-                         fwd_order=_heavy_first(row_cnt), bwd_order=bwd_order, slot_kb=slot_kb,
-                         slot_off=slot_off, slot_tiles=slot_tiles, pair_shared=pair_shared)
+                         fwd_order=fwd_order, bwd_order=bwd_order, slot_kb=slot_kb,
+                         slot_off=slot_off, slot_tiles=slot_tiles, pair_shared=pair_shared, **fp)
+
+
+def _fwd_pairs(row_off, row_tiles, row_cnt, fwd_order, nq, dev) -> dict:
+    """Pairs of consecutive heavy-first query blocks (bam_build_pair_lists over
+    the row lists): shared pairs run on CTA pairs (bam_attn_fwd_2cta), the
+    blocks of the other pairs as whole-row work items of the one-CTA kernel."""
+    npairs = (nq + 1) // 2
+    slot_q = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
+    slot_cnt = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
+    slot_off = torch.empty(2 * npairs + 1, dtype=torch.int32, device=dev)
+    shared = torch.empty(npairs, dtype=torch.int32, device=dev)
+    _lib.call("bam_build_pair_lists", row_off.data_ptr(), row_tiles.data_ptr(),
+              fwd_order.data_ptr(), nq, slot_q.data_ptr(), slot_cnt.data_ptr(),
+              slot_off.data_ptr(), None, shared.data_ptr())
+    slot_tiles = torch.empty(max(int(slot_off[-1].item()), 1), dtype=torch.int32, device=dev)
+    _lib.call("bam_build_pair_lists", row_off.data_ptr(), row_tiles.data_ptr(),
+              fwd_order.data_ptr(), nq, slot_q.data_ptr(), slot_cnt.data_ptr(),
+              slot_off.data_ptr(), slot_tiles.data_ptr(), shared.data_ptr())
+    sh = shared.bool()
+    pair_ids = torch.nonzero(sh).flatten().to(torch.int32)
+    rest = slot_q.view(npairs, 2)[~sh].flatten()
+    rest = rest[rest >= 0].to(torch.int64)
+    items = torch.stack([rest, torch.zeros_like(rest), row_cnt.to(torch.int64)[rest],
+                         torch.full_like(rest, -1)], dim=1).to(torch.int32).contiguous()
+    return dict(fwd_pair_ids=pair_ids, fwd_slot_q=slot_q, fwd_slot_off=slot_off,
+                fwd_slot_tiles=slot_tiles, fwd_rest_items=items)
 
 
 def plan_for_mask(mask: BitfieldMask) -> AttentionPlan:
@@ -225,6 +260,21 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         part_o.data_ptr() if part_o is not None else None,
         part_ml.data_ptr() if part_ml is not None else None,
         schedule.n_items if schedule is not None else 0, 0)
+    if (schedule is None and plan.fwd_pair_ids is not None and (nh // Hkv) % 2 == 0
+            and os.environ.get("BAM_FWD_2CTA", "0") == "1"):
+        # shared query-block pairs on CTA pairs, the rest as whole-row items.  Opt-in:
+        # measured 1084-1106 vs 1137-1143 TFLOP/s for the one-CTA head-pair kernel on
+        # config 4 -- the forward is bound by MUFU / softmax latency, not by the K/V
+        # operand traffic the CTA pair halves (profiles/r01/fwd_2cta.md)
+        n_pairs = int(plan.fwd_pair_ids.shape[0])
+        _lib.call("bam_attn_fwd_2cta", p, plan.fwd_pair_ids.data_ptr(), n_pairs,
+                  plan.fwd_slot_q.data_ptr(), plan.fwd_slot_off.data_ptr(),
+                  plan.fwd_slot_tiles.data_ptr())
+        n_rest = int(plan.fwd_rest_items.shape[0])
+        if n_rest:
+            p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
+            _lib.call("bam_attn_fwd", p)
+        return o, lse
     _lib.call("bam_attn_fwd", p)
     if schedule is not None and schedule.combine.shape[0]:
         _lib.call("bam_attn_fwd_combine", p, schedule.combine.data_ptr(),

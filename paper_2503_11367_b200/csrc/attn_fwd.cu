@@ -94,7 +94,8 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
                                              uint32_t colS, uint32_t colO, uint64_t* bar_s_full,
                                              uint64_t* bar_p_ready, uint64_t* bar_pv_done, int j,
                                              int h, uint32_t warp, uint32_t lane,
-                                             const int32_t* tiles, int n, int slot) {
+                                             const int32_t* tiles, int n, int slot,
+                                             uint32_t p_ready_remote = 0) {
   const int r = (warp & 3) * 32 + lane;
   const uint32_t lane_base = ((warp & 3) * 32) << 16;
   const long long qg = (long long)p.q_gid[j] * 128 + r;
@@ -111,6 +112,10 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
 #pragma unroll
     for (int c = 0; c < 4; ++c) BAM_TMEM_LD32(tmem + lane_base + colS + c * 32, (sr + c * 32));
     tmem_wait_ld();
+    if (cls == 0) {  // a tile only the other CTA of a pair sees: fully masked here
+#pragma unroll
+      for (int i = 0; i < 128; ++i) sr[i] = 0xff800000u;
+    }
     if (cls == 2) {  // PARTIAL: descriptor predicate per element, 32 columns at a time
       const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
 #pragma unroll
@@ -181,7 +186,12 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
     }
     tmem_wait_st();
     tc_fence_before();
-    mbar_arrive(bar_p_ready);
+    if (p_ready_remote) {  // the pair leader's barrier: one arrival per warp
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(p_ready_remote);
+    } else {
+      mbar_arrive(bar_p_ready);
+    }
   }
   // epilogue of a split-KV subblock: unnormalised fp32 O and (m, l) for the combine
   if (slot >= 0) {
@@ -496,6 +506,177 @@ __global__ void __maxnreg__(168)
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair (cta_group::2) head-pair kernel: a cluster of two CTAs = two query
+// blocks whose key-tile lists are (nearly) the same (the union list of a
+// "shared" pair from bam_build_pair_lists; a tile only one of them sees is
+// class 0 = fully masked for the other) x two query heads.  The even CTA
+// issues M = 256 MMAs: Q rows come from each CTA's own shared memory, K / V
+// are split by N -- each CTA loads 64 keys of K and 64 head-dim columns of V
+// per tile, half of the one-CTA kernel's K/V traffic, and each SM's shared
+// memory feeds 160 KB per key tile instead of 256 KB (tensor time 2048 clk).
+// Softmax / epilogue are the one-CTA kernel's, per CTA on its own TMEM rows.
+constexpr int k2Stages = 3;
+constexpr uint32_t kHalfTile = kTileBytes / 2;   // 64 keys x 128 d, or 128 keys x 64 d
+
+struct Pair2Smem {
+  alignas(1024) uint8_t q[2][kTileBytes];
+  alignas(1024) uint8_t k[k2Stages][kHalfTile];  // this CTA's 64 keys: two 64-col boxes of 8 KB
+  alignas(1024) uint8_t v[k2Stages][kHalfTile];  // this CTA's 64 d-columns of all 128 keys
+  uint64_t bar_q, bar_k_full[k2Stages], bar_k_empty[k2Stages], bar_v_full[k2Stages],
+      bar_v_empty[k2Stages];
+  uint64_t bar_s_full[2], bar_p_ready[2], bar_pv_done[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __maxnreg__(168)
+    attn_fwd_2cta_kernel(const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_k64,
+                         const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p,
+                         const int32_t* __restrict__ pair_ids, const int32_t* __restrict__ slot_q,
+                         const int32_t* __restrict__ slot_off,
+                         const int32_t* __restrict__ slot_tiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Pair2Smem& sm = *reinterpret_cast<Pair2Smem*>(smem_raw);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t crank = cluster_ctarank();
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  const int h0 = p.h_begin + 2 * blockIdx.y;
+  const int slot = 2 * pair_ids[blockIdx.x >> 1] + (int)crank;
+  const int j = slot_q[slot];
+  const int32_t* tiles = slot_tiles + slot_off[slot];
+  const int n = slot_off[slot + 1] - slot_off[slot];  // equal in both CTAs (union list)
+  const int hkv = (h0 - p.h_begin) / (nh / p.Hkv);
+
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+    mbar_init(&sm.bar_q, 1);
+    for (int i = 0; i < k2Stages; ++i) {
+      mbar_init(&sm.bar_k_full[i], 1);
+      mbar_init(&sm.bar_k_empty[i], 1);
+      mbar_init(&sm.bar_v_full[i], 1);
+      mbar_init(&sm.bar_v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.bar_s_full[i], 1);
+      mbar_init(&sm.bar_p_ready[i], 128 + 4);  // own warpgroup i per thread + the peer's per warp
+      mbar_init(&sm.bar_pv_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) {
+    tmem_alloc_2cta(&sm.tmem_base, 512);
+    tmem_relinquish_2cta();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers initialised before any remote signal
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    const uint32_t leader = elect_one();
+    if (n > 0) {
+      if (leader) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k64);
+        prefetch_tmap(&tm_v);
+      }
+      if (crank == 0) mbar_expect_tx_w(&sm.bar_q, 4 * kTileBytes, leader);
+      const uint32_t lbar_q = mapa_shared(smem_u32(&sm.bar_q), 0);
+      for (int i = 0; i < 2; ++i) {
+        tma_load_3d_2cta_w(&tm_q, lbar_q, sm.q[i], 0, h0 + i, j * 128, leader);
+        tma_load_3d_2cta_w(&tm_q, lbar_q, sm.q[i] + kTileBytes / 2, 64, h0 + i, j * 128, leader);
+      }
+      for (int t = 0; t < n; ++t) {
+        const int st = t % k2Stages;
+        const int krow = p.k_row[tiles[t] >> 2] * 128;
+        if (t >= k2Stages) mbar_wait_sleep(&sm.bar_k_empty[st], ((t / k2Stages) - 1) & 1);
+        if (crank == 0) mbar_expect_tx_w(&sm.bar_k_full[st], 2 * kHalfTile, leader);
+        const uint32_t lbar_k = mapa_shared(smem_u32(&sm.bar_k_full[st]), 0);
+        tma_load_3d_2cta_w(&tm_k64, lbar_k, sm.k[st], 0, hkv, krow + 64 * (int)crank, leader);
+        tma_load_3d_2cta_w(&tm_k64, lbar_k, sm.k[st] + kHalfTile / 2, 64, hkv,
+                           krow + 64 * (int)crank, leader);
+        if (t >= k2Stages) mbar_wait_sleep(&sm.bar_v_empty[st], ((t / k2Stages) - 1) & 1);
+        if (crank == 0) mbar_expect_tx_w(&sm.bar_v_full[st], 2 * kHalfTile, leader);
+        tma_load_3d_2cta_w(&tm_v, mapa_shared(smem_u32(&sm.bar_v_full[st]), 0), sm.v[st],
+                           64 * (int)crank, hkv, krow, leader);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer (even CTA)
+    const uint32_t leader = elect_one() && crank == 0;
+    if (n > 0 && crank == 0) {
+      const uint32_t idesc_s = idesc_bf16(256, 128, 0, 0);
+      const uint32_t idesc_o = idesc_bf16(256, 128, 0, 1);
+      const uint64_t dq0 = sdesc_sw128(smem_u32(sm.q[0]), 16, 1024);
+      const uint64_t dk0 = sdesc_sw128(smem_u32(sm.k[0]), 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(smem_u32(sm.v[0]), 16, 1024);
+      constexpr uint32_t kTile16 = kTileBytes >> 4, kHalf16 = kHalfTile >> 4;
+      auto issue_s = [&](int i, int t) {  // S_i(t) = Q_i K(t)^T, M = 256 over the pair
+        const uint64_t dq = dq0 + i * kTile16, dk = dk0 + (t % k2Stages) * kHalf16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t oq = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
+          const uint32_t ok = ((kk >> 2) * (kHalfTile / 2) + (kk & 3) * 32) >> 4;
+          mma_ss_2cta_w(tmem + 128 * i, dq + oq, dk + ok, idesc_s, kk > 0, leader);
+        }
+        tc_commit_2cta_mc_w(&sm.bar_s_full[i], 0x3, leader);
+      };
+      auto issue_pv = [&](int i, int t) {  // O_i += P_i(t) V(t), P_i bf16 in the S_i columns
+        const uint64_t dv = dv0 + (t % k2Stages) * kHalf16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts_2cta_w(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, dv + kk * 128, idesc_o,
+                        (t > 0 || kk > 0), leader);
+        tc_commit_2cta_mc_w(&sm.bar_pv_done[i], 0x3, leader);
+      };
+      mbar_wait(&sm.bar_q, 0);
+      mbar_wait(&sm.bar_k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      tc_commit_2cta_mc_w(&sm.bar_k_empty[0], 0x3, leader);
+      for (int t = 0; t < n; ++t) {
+        const int st = t % k2Stages, st1 = (t + 1) % k2Stages;
+        mbar_wait(&sm.bar_p_ready[0], t & 1);
+        mbar_wait(&sm.bar_v_full[st], (t / k2Stages) & 1);
+        tc_fence_after();
+        issue_pv(0, t);
+        if (t + 1 < n) {
+          mbar_wait(&sm.bar_k_full[st1], ((t + 1) / k2Stages) & 1);
+          tc_fence_after();
+          issue_s(0, t + 1);
+        }
+        mbar_wait(&sm.bar_p_ready[1], t & 1);
+        tc_fence_after();
+        issue_pv(1, t);
+        tc_commit_2cta_mc_w(&sm.bar_v_empty[st], 0x3, leader);
+        if (t + 1 < n) {
+          issue_s(1, t + 1);
+          tc_commit_2cta_mc_w(&sm.bar_k_empty[st1], 0x3, leader);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int i = warp >> 2;
+    const uint32_t p_ready_remote =
+        crank == 0 ? 0u : mapa_shared(smem_u32(&sm.bar_p_ready[i]), 0);
+    softmax_role<BAM_FWD_POLY_PAIR>(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i],
+                                    &sm.bar_p_ready[i], &sm.bar_pv_done[i], j, h0 + i, warp, lane,
+                                    tiles, n, -1, p_ready_remote);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the leader's MMAs into this CTA's TMEM are complete
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc_2cta(tmem, 512);
+  }
+}
+
 // Aggregation kernel: merge the split-KV subblock partials
 // of a query block; one CTA per (combine record, head), thread = row.
 __global__ void __launch_bounds__(128) combine_kernel(const BamAttnFwdParams p,
@@ -592,6 +773,44 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
     const dim3 grid = fwd::kRowMajor ? dim3(rows, nh) : dim3(nh, rows);
     fwd::attn_fwd_kernel<<<grid, fwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, p);
   }
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+extern "C" int bam_attn_fwd_2cta(const BamAttnFwdParams* pp, const int32_t* pair_ids,
+                                 int32_t n_pairs, const int32_t* slot_q, const int32_t* slot_off,
+                                 const int32_t* slot_tiles, void* stream) {
+  BAM_CHECK_ARG(pp != nullptr && pair_ids && slot_q && slot_off && slot_tiles,
+                "bam_attn_fwd_2cta: null argument");
+  const BamAttnFwdParams& p = *pp;
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  BAM_CHECK_ARG(p.nq >= 1 && p.k_rows >= 1 && p.Hkv >= 1 && nh % p.Hkv == 0 &&
+                    (nh / p.Hkv) % 2 == 0 && p.h_begin >= 0 && p.h_begin + nh <= p.Hq,
+                "bam_attn_fwd_2cta: needs an even GQA group (nh=%d Hkv=%d)", nh, p.Hkv);
+  BAM_CHECK_ARG(n_pairs >= 0, "bam_attn_fwd_2cta: n_pairs=%d", n_pairs);
+  if (n_pairs == 0) return kOk;
+  CUtensorMap mq, mk64, mv;
+  int rc;
+  if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mk64, p.k, (int64_t)p.k_rows * 128, p.Hkv, 64))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  const int smem = (int)sizeof(fwd::Pair2Smem);
+  BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_2cta_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * n_pairs, nh / 2);
+  cfg.blockDim = dim3(fwd::kPairThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BAM_CUDA_TRY(cudaLaunchKernelEx(&cfg, fwd::attn_fwd_2cta_kernel, mq, mk64, mv, p, pair_ids,
+                                  slot_q, slot_off, slot_tiles));
   BAM_LAUNCH_CHECK();
   return kOk;
 }

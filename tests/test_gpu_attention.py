@@ -196,3 +196,35 @@ def test_split_kv_schedule_matches_whole_rows(subblock):
         sizes = (sched.items[:, 2] - sched.items[:, 1]).cpu().tolist()
         assert sizes == sorted(sizes, reverse=True)
         assert max(sizes) <= subblock
+
+
+def test_fwd_cta_pair_kernel_matches_one_cta():
+    """The cta_group::2 forward (shared query-block pairs, union tile lists,
+    K/V split across the two SMs) against the one-CTA head-pair kernel."""
+    import os
+    from paper_2503_11367_b200 import attention as A, mask as M
+
+    segs = [("text", 384), ("img0", 512), ("text", 256), ("img1", 1024), ("text", 640)]
+    mask = M.build_bitfield(segs)
+    plan = A.plan_for_mask(mask)
+    assert plan.fwd_pair_ids.numel() > 0          # some pairs run on CTA pairs
+    T, Hq, Hkv = len(mask), 8, 2
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(21)
+    q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    old = os.environ.get("BAM_FWD_2CTA")
+    try:
+        os.environ["BAM_FWD_2CTA"] = "0"
+        o1, l1 = A.attn_forward(q, k, v, plan)
+        os.environ["BAM_FWD_2CTA"] = "1"
+        o2, l2 = A.attn_forward(q, k, v, plan)
+    finally:
+        if old is None:
+            os.environ.pop("BAM_FWD_2CTA", None)
+        else:
+            os.environ["BAM_FWD_2CTA"] = old
+    torch.cuda.synchronize()
+    assert (o1.float() - o2.float()).abs().max().item() < 1e-2
+    assert (l1 - l2).abs().max().item() < 1e-3
