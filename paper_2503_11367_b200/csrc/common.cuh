@@ -297,34 +297,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-// arrive (release at cluster scope) on an mbarrier of another CTA of the cluster
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
 // remote arrive with the default (CTA-scope) semantics: orders this thread's
 // tcgen05 work (after tcgen05.wait + fence::before_thread_sync) without the
 // GPU-scope memory barrier a cluster-scope release compiles to
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-// wait with cluster-scope acquire: the peer's remote stores before its arrive are visible
-template <int kSleepNs = 32>
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  uint32_t iters = 0, ok = 0;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P;\n\t}\n"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (ok) break;
-    if constexpr (kSleepNs > 0) __nanosleep(kSleepNs);
-    if (++iters > (1u << 28)) mbar_timeout_trap();
-  }
 }
 // ---- CTA-pair (cta_group::2) tensor-core helpers -----------------------------
 // One MMA issued by the even CTA of a cluster pair computes an M = 256 tile:
@@ -426,13 +403,6 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),        \
         "=r"(r[31])                                                                          \
       : "r"(taddr))
-
-#define BAM_TMEM_ST8(taddr, r)                                                                 \
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"( \
-                   taddr),                                                                     \
-               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),     \
-               "r"(r[7])                                                                       \
-               : "memory")
 
 #define BAM_TMEM_ST16(taddr, r)                                                           \
   asm volatile(                                                                           \
