@@ -266,9 +266,20 @@ def main():
 
     mk = lambda: [torch.cuda.Event(enable_timing=True)  # noqa: E731
                   for _ in range(3 + 2 * n_groups)]
-    for _ in range(args.warmup):
-        step(mk())
-    barrier()
+    try:
+        for _ in range(args.warmup):
+            step(mk())
+        barrier()
+    except Exception as exc:  # noqa: BLE001
+        if world == 1 or args.transport != "ce":
+            raise
+        # the copy-engine transport failed on this box: NCCL collectives instead
+        print(f"bench: copy-engine transport failed in warm-up ({exc}); using NCCL",
+              file=sys.stderr)
+        args.transport = "nccl"
+        for _ in range(args.warmup):
+            step(mk())
+        barrier()
     evs = [mk() for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.launch_count
