@@ -99,37 +99,43 @@ __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t
   const int r = (warp & 3) * 32 + lane;
   const uint32_t lane_base = ((warp & 3) * 32) << 16;
   const long long qg = (long long)p.q_gid[j] * 128 + r;
-  const long long dq = p.desc[qg];
   const float scale_log2 = p.scale * 1.4426950408889634f;
   float m = -INFINITY, l = 0.f;
   for (int t = 0; t < n; ++t) {
     const int e = tiles[t];
     const int cls = e & 3;
     const long long kg0 = (long long)(e >> 2) * 128;
+    // allow bits first (descriptors only): overlaps the wait for S(t) and keeps the
+    // predicate's temporaries out of the S row's live range
+    uint32_t bits[4] = {~0u, ~0u, ~0u, ~0u};
+    if (cls == 2) {  // PARTIAL: descriptor predicate per element, 32 columns at a time
+      const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
+      const long long dq = __ldg(reinterpret_cast<const long long*>(p.desc) + qg);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t b = 0;
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+          const long long d = __ldg(dk + c * 32 + i);
+          b |= uint32_t(bam_allowed(dq, qg, d, kg0 + c * 32 + i)) << i;
+        }
+        bits[c] = b;
+      }
+    } else if (cls == 0) {  // a tile only the other CTA of a pair sees: fully masked here
+      bits[0] = bits[1] = bits[2] = bits[3] = 0u;
+    }
     mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(bar_s_full, t & 1);
     tc_fence_after();
     uint32_t sr[128];  // S row as fp32 bits: four TMEM loads in flight, one wait
 #pragma unroll
     for (int c = 0; c < 4; ++c) BAM_TMEM_LD32(tmem + lane_base + colS + c * 32, (sr + c * 32));
     tmem_wait_ld();
-    if (cls == 0) {  // a tile only the other CTA of a pair sees: fully masked here
+    if (cls != 1) {
 #pragma unroll
-      for (int i = 0; i < 128; ++i) sr[i] = 0xff800000u;
-    }
-    if (cls == 2) {  // PARTIAL: descriptor predicate per element, 32 columns at a time
-      const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t bits = 0;
-#pragma unroll 4
-        for (int i = 0; i < 32; ++i) {
-          const long long d = __ldg(dk + c * 32 + i);
-          bits |= uint32_t(bam_allowed(dq, qg, d, kg0 + c * 32 + i)) << i;
-        }
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (!((bits >> i) & 1)) sr[c * 32 + i] = 0xff800000u;  // -inf
-      }
+          if (!((bits[c] >> i) & 1)) sr[c * 32 + i] = 0xff800000u;  // -inf
     }
     // row max: eight independent FMNMX3 chains instead of one serial chain
     float mx[8];
