@@ -513,6 +513,334 @@ __global__ void __maxnreg__(168)
 }
 
 // ---------------------------------------------------------------------------
+// Split-row softmax: TWO threads per query row (warps q and q+4 of a head's
+// eight softmax warps share TMEM lane quadrant q; thread half hf owns S / O
+// columns [64 hf, 64 hf + 64)).  Each thread carries 64 S values instead of
+// 128, so (a) a head-tile's 128 exponentials per row run on two warps' MUFU
+// turns, halving the softmax latency the MMA ping-pong must hide, and (b) the
+// row fits in ~100 registers.  The row max is combined through shared memory
+// (one 64-thread named barrier per tile); both threads then make the same
+// rescale decision.
+template <int kPolyEvery>
+__device__ __forceinline__ void softmax_half_role(
+    const BamAttnFwdParams& p, uint32_t tmem, uint32_t colS, uint32_t colO, uint64_t* bar_s_full,
+    uint64_t* bar_p_ready, uint64_t* bar_pv_done, int j, int h, uint32_t lw, uint32_t lane,
+    const int32_t* tiles, int n, int slot, float* xch /* [2][2][128] */, uint32_t bar_id) {
+  const uint32_t q = lw & 3, hf = lw >> 2;
+  const int r = q * 32 + lane;
+  const uint32_t lane_base = (q * 32) << 16;
+  const uint32_t cS = colS + 64 * hf, cP = colS + 32 * hf, cO = colO + 64 * hf;
+  const long long qg = (long long)p.q_gid[j] * 128 + r;
+  const float scale_log2 = p.scale * 1.4426950408889634f;
+  float m = -INFINITY, l = 0.f;
+  for (int t = 0; t < n; ++t) {
+    const int e = tiles[t];
+    const int cls = e & 3;
+    const long long kg0 = (long long)(e >> 2) * 128 + 64 * hf;
+    uint32_t bits[2] = {~0u, ~0u};
+    if (cls == 2) {
+      const long long* dk = reinterpret_cast<const long long*>(p.desc) + kg0;
+      const long long dq = __ldg(reinterpret_cast<const long long*>(p.desc) + qg);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t b = 0;
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+          const long long d = __ldg(dk + c * 32 + i);
+          b |= uint32_t(bam_allowed(dq, qg, d, kg0 + c * 32 + i)) << i;
+        }
+        bits[c] = b;
+      }
+    } else if (cls == 0) {
+      bits[0] = bits[1] = 0u;
+    }
+    mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(bar_s_full, t & 1);
+    tc_fence_after();
+    uint32_t sr[64];
+    BAM_TMEM_LD32(tmem + lane_base + cS, sr);
+    BAM_TMEM_LD32(tmem + lane_base + cS + 32, (sr + 32));
+    tmem_wait_ld();
+    if (cls != 1) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (!((bits[c] >> i) & 1)) sr[c * 32 + i] = 0xff800000u;
+    }
+    float mx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      mx[k] = fmaxf(__uint_as_float(sr[2 * k]), __uint_as_float(sr[2 * k + 1]));
+#pragma unroll
+    for (int c = 8; c < 64; c += 8)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mx[k] = fmaxf(mx[k], fmaxf(__uint_as_float(sr[c + 2 * k]), __uint_as_float(sr[c + 2 * k + 1])));
+    float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+    // combine with the other half of the row (double-buffered by tile parity); the
+    // barrier also orders the partner's S loads before this thread's P stores
+    float* xb = xch + (t & 1) * 256;
+    xb[hf * 128 + r] = mt;
+    named_bar_sync(bar_id, 64);
+    mt = fmaxf(mt, xb[(hf ^ 1) * 128 + r]);
+    const float m_new = fmaxf(m, mt * scale_log2);
+    const bool rescale = m_new > m + 8.f;
+    const float alpha = rescale ? ex2(m - m_new) : 1.f;
+    if (rescale) {
+      l *= alpha;
+      m = m_new;
+    }
+    const float mb = (m == -INFINITY) ? 0.f : m;
+    const float2 sc2 = make_float2(scale_log2, scale_log2), nmb2 = make_float2(-mb, -mb);
+    float2 ls = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 x = ffma2(make_float2(__uint_as_float(sr[c * 32 + 2 * i]),
+                                           __uint_as_float(sr[c * 32 + 2 * i + 1])),
+                               sc2, nmb2);
+        const float2 pp = (kPolyEvery > 0 && (c * 16 + i) % (kPolyEvery > 0 ? kPolyEvery : 1) ==
+                                                 kPolyEvery - 1)
+                              ? ex2_poly2(x)
+                              : make_float2(ex2(x.x), ex2(x.y));
+        ls = fadd2(ls, pp);
+        pk[i] = pack_bf16(pp.x, pp.y);
+      }
+      BAM_TMEM_ST16(tmem + lane_base + cP + c * 16, pk);
+    }
+    l += ls.x + ls.y;
+    if (__any_sync(0xffffffffu, rescale) && t > 0) {
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t rr[32];
+        BAM_TMEM_LD32(tmem + lane_base + cO + c * 32, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+        BAM_TMEM_ST32(tmem + lane_base + cO + c * 32, rr);
+      }
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    mbar_arrive(bar_p_ready);
+  }
+  // row sum of both halves (same m in both threads)
+  xch[512 + hf * 128 + r] = l;
+  named_bar_sync(bar_id, 64);
+  const float l_row = l + xch[512 + (hf ^ 1) * 128 + r];
+  if (slot >= 0) {  // split-KV subblock: unnormalised fp32 O and (m, l)
+    float* po = p.part_o + (((int64_t)slot * p.Hq + h) * 128 + r) * 128 + 64 * hf;
+    if (n > 0) {
+      mbar_wait_sleep(bar_pv_done, (n - 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t rr[32];
+        BAM_TMEM_LD32(tmem + lane_base + cO + c * 32, rr);
+        tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(po + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(__uint_as_float(rr[4 * i]), __uint_as_float(rr[4 * i + 1]),
+                               __uint_as_float(rr[4 * i + 2]), __uint_as_float(rr[4 * i + 3]));
+      }
+    } else {
+      for (int i = 0; i < 16; ++i) reinterpret_cast<float4*>(po)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (hf == 0)
+      reinterpret_cast<float2*>(p.part_ml)[((int64_t)slot * p.Hq + h) * 128 + r] =
+          make_float2(n > 0 ? m : -INFINITY, n > 0 ? l_row : 0.f);
+    return;
+  }
+  const int64_t Tq = (int64_t)p.nq * 128;
+  const int64_t row = (int64_t)j * 128 + r;
+  __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + (row * p.Hq + h) * 128 + 64 * hf;
+  if (n > 0) {
+    mbar_wait_sleep(bar_pv_done, (n - 1) & 1);
+    tc_fence_after();
+    const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t rr[32];
+      BAM_TMEM_LD32(tmem + lane_base + cO + c * 32, rr);
+      tmem_wait_ld();
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 v;
+        v.x = pack_bf16(__uint_as_float(rr[8 * i + 0]) * inv, __uint_as_float(rr[8 * i + 1]) * inv);
+        v.y = pack_bf16(__uint_as_float(rr[8 * i + 2]) * inv, __uint_as_float(rr[8 * i + 3]) * inv);
+        v.z = pack_bf16(__uint_as_float(rr[8 * i + 4]) * inv, __uint_as_float(rr[8 * i + 5]) * inv);
+        v.w = pack_bf16(__uint_as_float(rr[8 * i + 6]) * inv, __uint_as_float(rr[8 * i + 7]) * inv);
+        dst[i] = v;
+      }
+    }
+    if (hf == 0)
+      p.lse[(int64_t)h * Tq + row] =
+          l_row > 0.f ? (m + __log2f(l_row)) * 0.6931471805599453f : -INFINITY;
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(orow);
+    for (int i = 0; i < 8; ++i) dst[i] = make_uint4(0, 0, 0, 0);
+    if (hf == 0) p.lse[(int64_t)h * Tq + row] = -INFINITY;
+  }
+}
+
+// GQA head-pair kernel with split-row softmax: 16 softmax warps (8 per head:
+// 2 per TMEM lane quadrant), warp 16 TMA, warp 17 MMA; otherwise the
+// head-pair kernel above (same TMEM layout, ping-pong and K/V ring).
+constexpr int kSplitThreads = 576;
+#ifndef BAM_FWD_SPLIT
+#define BAM_FWD_SPLIT 1
+#endif
+#ifndef BAM_FWD_POLY_SPLIT
+#define BAM_FWD_POLY_SPLIT 4
+#endif
+
+struct SplitSmem {
+  alignas(1024) uint8_t q[2][kTileBytes];
+  alignas(1024) uint8_t k[2][kTileBytes];
+  alignas(1024) uint8_t v[2][kTileBytes];
+  float xch[2][768];  // per head: max exchange [2 parity][2 halves][128] + row sums [2][128]
+  uint64_t bar_q, bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
+  uint64_t bar_s_full[2], bar_p_ready[2], bar_pv_done[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kSplitThreads, 1)
+    attn_fwd_split_kernel(const __grid_constant__ CUtensorMap tm_q,
+                          const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem_raw);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  const int h0 = p.h_begin + 2 * (kRowMajor ? blockIdx.y : blockIdx.x);
+  const WorkItem wi = work_item(p, kRowMajor ? blockIdx.x : blockIdx.y);
+  const int j = wi.j, n = wi.n, slot = wi.slot;
+  const int32_t* tiles = wi.tiles;
+  const int hkv = (h0 - p.h_begin) / (nh / p.Hkv);
+  constexpr uint32_t kWarpTma = 16, kWarpMma = 17;
+
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem_raw) & 1023) != 0) __trap();
+    mbar_init(&sm.bar_q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.bar_k_full[i], 1);
+      mbar_init(&sm.bar_k_empty[i], 1);
+      mbar_init(&sm.bar_v_full[i], 1);
+      mbar_init(&sm.bar_v_empty[i], 1);
+      mbar_init(&sm.bar_s_full[i], 1);
+      mbar_init(&sm.bar_p_ready[i], 256);
+      mbar_init(&sm.bar_pv_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kWarpMma) {
+    tmem_alloc(&sm.tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == kWarpTma) {
+    const uint32_t leader = elect_one();
+    if (n > 0) {
+      if (leader) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+      }
+      mbar_expect_tx_w(&sm.bar_q, 2 * kTileBytes, leader);
+      for (int i = 0; i < 2; ++i) {
+        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i], 0, h0 + i, j * 128, leader);
+        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i] + kTileBytes / 2, 64, h0 + i, j * 128, leader);
+      }
+      for (int t = 0; t < n; ++t) {
+        const int st = t & 1;
+        const int krow = p.k_row[tiles[t] >> 2] * 128;
+        if (t >= 2) mbar_wait_sleep(&sm.bar_k_empty[st], ((t >> 1) - 1) & 1);
+        mbar_expect_tx_w(&sm.bar_k_full[st], kTileBytes, leader);
+        tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st], 0, hkv, krow, leader);
+        tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st] + kTileBytes / 2, 64, hkv, krow, leader);
+        if (t >= 2) mbar_wait_sleep(&sm.bar_v_empty[st], ((t >> 1) - 1) & 1);
+        mbar_expect_tx_w(&sm.bar_v_full[st], kTileBytes, leader);
+        tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st], 0, hkv, krow, leader);
+        tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st] + kTileBytes / 2, 64, hkv, krow, leader);
+      }
+    }
+  } else if (warp == kWarpMma) {
+    const uint32_t leader = elect_one();
+    if (n > 0) {
+      const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      const uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
+      const uint64_t dq0 = sdesc_sw128(smem_u32(sm.q[0]), 16, 1024);
+      const uint64_t dk0 = sdesc_sw128(smem_u32(sm.k[0]), 16, 1024);
+      const uint64_t dv0 = sdesc_sw128(smem_u32(sm.v[0]), kTileBytes / 2, 1024);
+      constexpr uint32_t kTile16 = kTileBytes >> 4;
+      auto issue_s = [&](int i, int t) {
+        const uint64_t dq = dq0 + i * kTile16, dk = dk0 + (t & 1) * kTile16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
+          mma_ss_w(tmem + 128 * i, dq + off, dk + off, idesc_s, kk > 0, leader);
+        }
+        tc_commit_w(&sm.bar_s_full[i], leader);
+      };
+      auto issue_pv = [&](int i, int t) {
+        const uint64_t dv = dv0 + (t & 1) * kTile16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts_w(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, dv + kk * 128, idesc_o,
+                   (t > 0 || kk > 0), leader);
+        tc_commit_w(&sm.bar_pv_done[i], leader);
+      };
+      mbar_wait(&sm.bar_q, 0);
+      mbar_wait(&sm.bar_k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      tc_commit_w(&sm.bar_k_empty[0], leader);
+      for (int t = 0; t < n; ++t) {
+        const int st = t & 1, st1 = (t + 1) & 1;
+        mbar_wait(&sm.bar_p_ready[0], t & 1);
+        mbar_wait(&sm.bar_v_full[st], (t >> 1) & 1);
+        tc_fence_after();
+        issue_pv(0, t);
+        if (t + 1 < n) {
+          mbar_wait(&sm.bar_k_full[st1], ((t + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(0, t + 1);
+        }
+        mbar_wait(&sm.bar_p_ready[1], t & 1);
+        tc_fence_after();
+        issue_pv(1, t);
+        tc_commit_w(&sm.bar_v_empty[st], leader);
+        if (t + 1 < n) {
+          issue_s(1, t + 1);
+          tc_commit_w(&sm.bar_k_empty[st1], leader);
+        }
+      }
+    }
+  } else {
+    const int i = warp >> 3;  // head: warps 0-7 / 8-15
+    const uint32_t lw = warp & 7;
+    softmax_half_role<BAM_FWD_POLY_SPLIT>(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i],
+                                          &sm.bar_p_ready[i], &sm.bar_pv_done[i], j, h0 + i, lw,
+                                          lane, tiles, n, slot, sm.xch[i], 1 + i * 4 + (lw & 3));
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CTA-pair (cta_group::2) head-pair kernel: a cluster of two CTAs = two query
 // blocks whose key-tile lists are (nearly) the same (the union list of a
 // "shared" pair from bam_build_pair_lists; a tile only one of them sees is
@@ -763,7 +1091,15 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
   if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
   const int grp = nh / p.Hkv;
-  if (grp % 2 == 0) {  // GQA: two query heads share each K/V tile
+  if (grp % 2 == 0 && BAM_FWD_SPLIT) {  // GQA head pairs, split-row softmax
+    const int smem = (int)sizeof(fwd::SplitSmem);
+    BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_split_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int rows = p.items ? p.n_items : p.nq;
+    const dim3 grid = fwd::kRowMajor ? dim3(rows, nh / 2) : dim3(nh / 2, rows);
+    fwd::attn_fwd_split_kernel<<<grid, fwd::kSplitThreads, smem, (cudaStream_t)stream>>>(
+        mq, mk, mv, p);
+  } else if (grp % 2 == 0) {  // GQA: two query heads share each K/V tile
     const int smem = (int)sizeof(fwd::PairSmem);
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_pair_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
