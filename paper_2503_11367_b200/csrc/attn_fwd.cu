@@ -67,9 +67,9 @@ __device__ __forceinline__ WorkItem work_item(const BamAttnFwdParams& p, int y) 
 
 // One in kPolyEvery exponential PAIRS runs on the FMA pipe (ex2_poly2) so the MUFU
 // unit (16 ex2 / clk / SM) is not the softmax bottleneck.  Measured on B200:
-// the MHA kernel (two CTAs per SM) is fastest at 1 in 3, the GQA head-pair
-// kernel (two softmax warpgroups sharing each SM sub-partition's issue slots)
-// with none (config 4: 1090 vs 1040 TFLOP/s at 1 in 4).
+// the MHA kernel (two CTAs per SM) is fastest at 1 in 3; the CTA-pair kernel
+// (one softmax thread per row at its 168-register ceiling) with none; the
+// split-row head-pair kernel at 1 in 4 (BAM_FWD_POLY_SPLIT).
 #ifndef BAM_FWD_POLY_MHA
 #define BAM_FWD_POLY_MHA 3
 #endif
@@ -359,158 +359,16 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
-// GQA head-pair kernel: one CTA = one 128-row query block x two query heads of
-// the same KV group (identical tile lists and masks, shared K/V tiles), 1 CTA
-// per SM.  TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).  The MMA
-// warp ping-pongs the two tiles so one warpgroup's softmax overlaps the other
-// tile's MMAs:  S0(0) S1(0) | PV0(0) S0(1) | PV1(0) S1(1) | PV0(1) S0(2) | ...
-// K/V tiles stream through a 2-stage ring.
-//   warps 0-3 softmax tile 0, warps 4-7 softmax tile 1, warp 8 TMA, warp 9 MMA.
-// 168 registers is the ceiling at 320 threads (registers are allocated for
-// whole warpgroups: 12 x 32 x 168 = 64512; 176 fails to launch); the softmax
-// then spills a few loop invariants (~60 B / thread).
-constexpr int kPairThreads = 320;
-
-struct PairSmem {
-  alignas(1024) uint8_t q[2][kTileBytes];
-  alignas(1024) uint8_t k[2][kTileBytes];
-  alignas(1024) uint8_t v[2][kTileBytes];
-  uint64_t bar_q, bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
-  uint64_t bar_s_full[2], bar_p_ready[2], bar_pv_done[2];
-  uint32_t tmem_base;
-};
-
-__global__ void __maxnreg__(168)
-    attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q,
-                         const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const int nh = p.nh > 0 ? p.nh : p.Hq;
-  const int h0 = p.h_begin + 2 * (kRowMajor ? blockIdx.y : blockIdx.x);
-  const WorkItem wi = work_item(p, kRowMajor ? blockIdx.x : blockIdx.y);
-  const int j = wi.j, n = wi.n, slot = wi.slot;
-  const int32_t* tiles = wi.tiles;
-  const int hkv = (h0 - p.h_begin) / (nh / p.Hkv);
-
-  if (threadIdx.x == 0) {
-    if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B needs 1024-B alignment
-    mbar_init(&sm.bar_q, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.bar_k_full[i], 1);
-      mbar_init(&sm.bar_k_empty[i], 1);
-      mbar_init(&sm.bar_v_full[i], 1);
-      mbar_init(&sm.bar_v_empty[i], 1);
-      mbar_init(&sm.bar_s_full[i], 1);
-      mbar_init(&sm.bar_p_ready[i], 128);
-      mbar_init(&sm.bar_pv_done[i], 1);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 9) {
-    tmem_alloc(&sm.tmem_base, 512);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = sm.tmem_base;
-
-  if (warp == 8) {
-    // ------------------------------------------------------------ TMA producer (whole warp)
-    const uint32_t leader = elect_one();
-    if (n > 0) {
-      if (leader) {
-        prefetch_tmap(&tm_q);
-        prefetch_tmap(&tm_k);
-        prefetch_tmap(&tm_v);
-      }
-      mbar_expect_tx_w(&sm.bar_q, 2 * kTileBytes, leader);
-      for (int i = 0; i < 2; ++i) {
-        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i], 0, h0 + i, j * 128, leader);
-        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i] + kTileBytes / 2, 64, h0 + i, j * 128, leader);
-      }
-      for (int t = 0; t < n; ++t) {
-        const int st = t & 1;
-        const int krow = p.k_row[tiles[t] >> 2] * 128;
-        if (t >= 2) mbar_wait_sleep(&sm.bar_k_empty[st], ((t >> 1) - 1) & 1);
-        mbar_expect_tx_w(&sm.bar_k_full[st], kTileBytes, leader);
-        tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st], 0, hkv, krow, leader);
-        tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st] + kTileBytes / 2, 64, hkv, krow, leader);
-        if (t >= 2) mbar_wait_sleep(&sm.bar_v_empty[st], ((t >> 1) - 1) & 1);
-        mbar_expect_tx_w(&sm.bar_v_full[st], kTileBytes, leader);
-        tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st], 0, hkv, krow, leader);
-        tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st] + kTileBytes / 2, 64, hkv, krow, leader);
-      }
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer (whole warp)
-    const uint32_t leader = elect_one();
-    if (n > 0) {
-      const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
-      const uint32_t idesc_o = idesc_bf16(128, 128, 0, 1);
-      const uint64_t dq0 = sdesc_sw128(smem_u32(sm.q[0]), 16, 1024);
-      const uint64_t dk0 = sdesc_sw128(smem_u32(sm.k[0]), 16, 1024);
-      const uint64_t dv0 = sdesc_sw128(smem_u32(sm.v[0]), kTileBytes / 2, 1024);
-      constexpr uint32_t kTile16 = kTileBytes >> 4;
-      auto issue_s = [&](int i, int t) {  // S_i(t) = Q_i K(t)^T -> TMEM cols [128 i, +128)
-        const uint64_t dq = dq0 + i * kTile16, dk = dk0 + (t & 1) * kTile16;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
-          mma_ss_w(tmem + 128 * i, dq + off, dk + off, idesc_s, kk > 0, leader);
-        }
-        tc_commit_w(&sm.bar_s_full[i], leader);
-      };
-      auto issue_pv = [&](int i, int t) {  // O_i += P_i(t) V(t), P_i bf16 in the S_i columns
-        const uint64_t dv = dv0 + (t & 1) * kTile16;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts_w(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, dv + kk * 128, idesc_o,
-                   (t > 0 || kk > 0), leader);
-        tc_commit_w(&sm.bar_pv_done[i], leader);
-      };
-      mbar_wait(&sm.bar_q, 0);
-      mbar_wait(&sm.bar_k_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      tc_commit_w(&sm.bar_k_empty[0], leader);
-      for (int t = 0; t < n; ++t) {
-        const int st = t & 1, st1 = (t + 1) & 1;
-        mbar_wait(&sm.bar_p_ready[0], t & 1);
-        mbar_wait(&sm.bar_v_full[st], (t >> 1) & 1);
-        tc_fence_after();
-        issue_pv(0, t);
-        if (t + 1 < n) {  // S0(t+1) overwrites P0(t): issued after PV0(t), executes in order
-          mbar_wait(&sm.bar_k_full[st1], ((t + 1) >> 1) & 1);
-          tc_fence_after();
-          issue_s(0, t + 1);
-        }
-        mbar_wait(&sm.bar_p_ready[1], t & 1);
-        tc_fence_after();
-        issue_pv(1, t);
-        tc_commit_w(&sm.bar_v_empty[st], leader);
-        if (t + 1 < n) {
-          issue_s(1, t + 1);
-          tc_commit_w(&sm.bar_k_empty[st1], leader);
-        }
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax warpgroups
-    const int i = warp >> 2;  // tile 0: warps 0-3, tile 1: warps 4-7
-    softmax_role<BAM_FWD_POLY_PAIR>(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i], &sm.bar_p_ready[i],
-                 &sm.bar_pv_done[i], j, h0 + i, warp, lane, tiles, n, slot);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
+// GQA head pairs: one CTA = one 128-row query block x two query heads of the
+// same KV group (identical tile lists and masks, shared K/V tiles), 1 CTA per
+// SM.  TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).  The MMA warp
+// ping-pongs the two tiles so one head's softmax overlaps the other head's
+// MMAs:  S0(0) S1(0) | PV0(0) S0(1) | PV1(0) S1(1) | PV0(1) S0(2) | ...
+// K/V tiles stream through a 2-stage ring.  (A 320-thread variant with one
+// softmax thread per row sat at its 168-register launch ceiling -- registers
+// are allocated per warpgroup, 12 x 32 x 168 -- and spilled; the split-row
+// kernel below replaced it: config 4 forward 1125 -> 1220 TFLOP/s.)
+constexpr int kPairThreads = 320;   // the CTA-pair kernel's block size
 
 // ---------------------------------------------------------------------------
 // Split-row softmax: TWO threads per query row (warps q and q+4 of a head's
@@ -688,12 +546,8 @@ __device__ __forceinline__ void softmax_half_role(
 }
 
 // GQA head-pair kernel with split-row softmax: 16 softmax warps (8 per head:
-// 2 per TMEM lane quadrant), warp 16 TMA, warp 17 MMA; otherwise the
-// head-pair kernel above (same TMEM layout, ping-pong and K/V ring).
+// 2 per TMEM lane quadrant), warp 16 TMA, warp 17 MMA.
 constexpr int kSplitThreads = 576;
-#ifndef BAM_FWD_SPLIT
-#define BAM_FWD_SPLIT 1
-#endif
 #ifndef BAM_FWD_POLY_SPLIT
 #define BAM_FWD_POLY_SPLIT 4
 #endif
@@ -1091,7 +945,7 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
   if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
   const int grp = nh / p.Hkv;
-  if (grp % 2 == 0 && BAM_FWD_SPLIT) {  // GQA head pairs, split-row softmax
+  if (grp % 2 == 0) {  // GQA head pairs, split-row softmax
     const int smem = (int)sizeof(fwd::SplitSmem);
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_split_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1099,14 +953,6 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
     const dim3 grid = fwd::kRowMajor ? dim3(rows, nh / 2) : dim3(nh / 2, rows);
     fwd::attn_fwd_split_kernel<<<grid, fwd::kSplitThreads, smem, (cudaStream_t)stream>>>(
         mq, mk, mv, p);
-  } else if (grp % 2 == 0) {  // GQA: two query heads share each K/V tile
-    const int smem = (int)sizeof(fwd::PairSmem);
-    BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_pair_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int rows = p.items ? p.n_items : p.nq;
-    const dim3 grid = fwd::kRowMajor ? dim3(rows, nh / 2) : dim3(nh / 2, rows);
-    fwd::attn_fwd_pair_kernel<<<grid, fwd::kPairThreads, smem, (cudaStream_t)stream>>>(mq, mk,
-                                                                                       mv, p);
   } else {
     const int smem = (int)sizeof(fwd::Smem) + 1024;
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
