@@ -229,6 +229,16 @@ int bam_attn_fwd_2cta(const BamAttnFwdParams* p, const int32_t* pair_ids, int32_
                       const int32_t* slot_q, const int32_t* slot_off, const int32_t* slot_tiles,
                       void* stream);
 
+/* Forward on query-block pairs within one CTA (any head grouping, used for
+ * MHA): the shared pairs pair_ids of bam_build_pair_lists over the row lists
+ * run as one CTA per (pair, head) -- the two query blocks share every K/V
+ * tile and the split-row softmax -- with the union lists slot_tiles; the
+ * blocks of non-shared pairs go through bam_attn_fwd with a whole-row items
+ * list.  Whole rows only. */
+int bam_attn_fwd_qpairs(const BamAttnFwdParams* p, const int32_t* pair_ids, int32_t n_pairs,
+                        const int32_t* slot_q, const int32_t* slot_off, const int32_t* slot_tiles,
+                        void* stream);
+
 /* ---- token permutation ----------------- */
 /* The CP runtime permutes tokens into the LPT block layout before attention
  * and back afterwards.  Block-row gather / scatter for up to BAM_PERMUTE_MAX

@@ -275,6 +275,18 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
             p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
             _lib.call("bam_attn_fwd", p)
         return o, lse
+    if (schedule is None and plan.fwd_pair_ids is not None and (nh // Hkv) % 2 == 1
+            and os.environ.get("BAM_FWD_QPAIRS", "1") != "0"):
+        # MHA: shared query-block pairs share K/V tiles in one split-row CTA; the
+        # blocks of the other pairs run as whole-row items of the one-head kernel
+        _lib.call("bam_attn_fwd_qpairs", p, plan.fwd_pair_ids.data_ptr(),
+                  int(plan.fwd_pair_ids.shape[0]), plan.fwd_slot_q.data_ptr(),
+                  plan.fwd_slot_off.data_ptr(), plan.fwd_slot_tiles.data_ptr())
+        n_rest = int(plan.fwd_rest_items.shape[0])
+        if n_rest:
+            p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
+            _lib.call("bam_attn_fwd", p)
+        return o, lse
     _lib.call("bam_attn_fwd", p)
     if schedule is not None and schedule.combine.shape[0]:
         _lib.call("bam_attn_fwd_combine", p, schedule.combine.data_ptr(),

@@ -562,19 +562,46 @@ struct SplitSmem {
   uint32_t tmem_base;
 };
 
+// kQPair = false: tile i = head h0 + i of query block j (GQA head pair).
+// kQPair = true: tile i = query block slot_q[2 pr + i] of head h (MHA query-block
+// pair of bam_build_pair_lists' shared pairs: one union tile list, class 0 where
+// a block does not see the key tile), so the two tiles still share K/V.
+template <bool kQPair>
 __global__ void __launch_bounds__(kSplitThreads, 1)
     attn_fwd_split_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_k,
-                          const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p) {
+                          const __grid_constant__ CUtensorMap tm_v, const BamAttnFwdParams p,
+                          const int32_t* __restrict__ pair_ids, const int32_t* __restrict__ slot_q,
+                          const int32_t* __restrict__ slot_off,
+                          const int32_t* __restrict__ slot_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
-  const int h0 = p.h_begin + 2 * (kRowMajor ? blockIdx.y : blockIdx.x);
-  const WorkItem wi = work_item(p, kRowMajor ? blockIdx.x : blockIdx.y);
-  const int j = wi.j, n = wi.n, slot = wi.slot;
-  const int32_t* tiles = wi.tiles;
-  const int hkv = (h0 - p.h_begin) / (nh / p.Hkv);
+  const int bx = kRowMajor ? blockIdx.x : blockIdx.y, by = kRowMajor ? blockIdx.y : blockIdx.x;
+  int jj[2], hh[2], n, slot;
+  const int32_t* tl[2];
+  if constexpr (kQPair) {
+    const int pr = pair_ids[bx];
+    for (int i = 0; i < 2; ++i) {
+      jj[i] = slot_q[2 * pr + i];
+      hh[i] = p.h_begin + by;
+      tl[i] = slot_tiles + slot_off[2 * pr + i];
+    }
+    n = slot_off[2 * pr + 1] - slot_off[2 * pr];
+    slot = -1;
+  } else {
+    const WorkItem wi = work_item(p, bx);
+    for (int i = 0; i < 2; ++i) {
+      jj[i] = wi.j;
+      hh[i] = p.h_begin + 2 * by + i;
+      tl[i] = wi.tiles;
+    }
+    n = wi.n;
+    slot = wi.slot;
+  }
+  const int32_t* tiles = tl[0];   // the key-tile order (identical in both lists)
+  const int hkv = (hh[0] - p.h_begin) / (nh / p.Hkv);
   constexpr uint32_t kWarpTma = 16, kWarpMma = 17;
 
   if (threadIdx.x == 0) {
@@ -610,8 +637,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
       }
       mbar_expect_tx_w(&sm.bar_q, 2 * kTileBytes, leader);
       for (int i = 0; i < 2; ++i) {
-        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i], 0, h0 + i, j * 128, leader);
-        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i] + kTileBytes / 2, 64, h0 + i, j * 128, leader);
+        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i], 0, hh[i], jj[i] * 128, leader);
+        tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i] + kTileBytes / 2, 64, hh[i], jj[i] * 128, leader);
       }
       for (int t = 0; t < n; ++t) {
         const int st = t & 1;
@@ -683,8 +710,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     const int i = warp >> 3;  // head: warps 0-7 / 8-15
     const uint32_t lw = warp & 7;
     softmax_half_role<BAM_FWD_POLY_SPLIT>(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i],
-                                          &sm.bar_p_ready[i], &sm.bar_pv_done[i], j, h0 + i, lw,
-                                          lane, tiles, n, slot, sm.xch[i], 1 + i * 4 + (lw & 3));
+                                          &sm.bar_p_ready[i], &sm.bar_pv_done[i], jj[i], hh[i],
+                                          lw, lane, tl[i], n, slot, sm.xch[i],
+                                          1 + i * 4 + (lw & 3));
   }
   tc_fence_before();
   __syncthreads();
@@ -947,12 +975,12 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
   const int grp = nh / p.Hkv;
   if (grp % 2 == 0) {  // GQA head pairs, split-row softmax
     const int smem = (int)sizeof(fwd::SplitSmem);
-    BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_split_kernel,
+    BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_split_kernel<false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int rows = p.items ? p.n_items : p.nq;
     const dim3 grid = fwd::kRowMajor ? dim3(rows, nh / 2) : dim3(nh / 2, rows);
-    fwd::attn_fwd_split_kernel<<<grid, fwd::kSplitThreads, smem, (cudaStream_t)stream>>>(
-        mq, mk, mv, p);
+    fwd::attn_fwd_split_kernel<false><<<grid, fwd::kSplitThreads, smem, (cudaStream_t)stream>>>(
+        mq, mk, mv, p, nullptr, nullptr, nullptr, nullptr);
   } else {
     const int smem = (int)sizeof(fwd::Smem) + 1024;
     BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_kernel,
@@ -999,6 +1027,34 @@ extern "C" int bam_attn_fwd_2cta(const BamAttnFwdParams* pp, const int32_t* pair
   cfg.numAttrs = 1;
   BAM_CUDA_TRY(cudaLaunchKernelEx(&cfg, fwd::attn_fwd_2cta_kernel, mq, mk64, mv, p, pair_ids,
                                   slot_q, slot_off, slot_tiles));
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+extern "C" int bam_attn_fwd_qpairs(const BamAttnFwdParams* pp, const int32_t* pair_ids,
+                                   int32_t n_pairs, const int32_t* slot_q, const int32_t* slot_off,
+                                   const int32_t* slot_tiles, void* stream) {
+  BAM_CHECK_ARG(pp != nullptr && pair_ids && slot_q && slot_off && slot_tiles,
+                "bam_attn_fwd_qpairs: null argument");
+  const BamAttnFwdParams& p = *pp;
+  const int nh = p.nh > 0 ? p.nh : p.Hq;
+  BAM_CHECK_ARG(p.nq >= 1 && p.k_rows >= 1 && p.Hkv >= 1 && nh % p.Hkv == 0 && p.h_begin >= 0 &&
+                    p.h_begin + nh <= p.Hq,
+                "bam_attn_fwd_qpairs: head group [%d, %d) of Hq=%d over Hkv=%d", p.h_begin,
+                p.h_begin + nh, p.Hq, p.Hkv);
+  BAM_CHECK_ARG(n_pairs >= 0, "bam_attn_fwd_qpairs: n_pairs=%d", n_pairs);
+  if (n_pairs == 0) return kOk;
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  const int smem = (int)sizeof(fwd::SplitSmem);
+  BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_split_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const dim3 grid = fwd::kRowMajor ? dim3(n_pairs, nh) : dim3(nh, n_pairs);
+  fwd::attn_fwd_split_kernel<true><<<grid, fwd::kSplitThreads, smem, (cudaStream_t)stream>>>(
+      mq, mk, mv, p, pair_ids, slot_q, slot_off, slot_tiles);
   BAM_LAUNCH_CHECK();
   return kOk;
 }

@@ -228,3 +228,34 @@ def test_fwd_cta_pair_kernel_matches_one_cta():
     torch.cuda.synchronize()
     assert (o1.float() - o2.float()).abs().max().item() < 1e-2
     assert (l1 - l2).abs().max().item() < 1e-3
+
+
+def test_fwd_query_block_pairs_match_one_head_kernel():
+    """MHA forward on query-block pairs (split-row CTA sharing K/V tiles over
+    a union tile list) against the one-head kernel."""
+    import os
+    from paper_2503_11367_b200 import attention as A, mask as M
+
+    segs = [("text", 384), ("img0", 512), ("text", 256), ("img1", 1024), ("text", 640)]
+    mask = M.build_bitfield(segs)
+    plan = A.plan_for_mask(mask)
+    assert plan.fwd_pair_ids.numel() > 0
+    T, H = len(mask), 3
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(22)
+    q, k, v = (torch.randn(T, H, 128, device=dev, generator=g, dtype=torch.bfloat16)
+               for _ in range(3))
+    old = os.environ.get("BAM_FWD_QPAIRS")
+    try:
+        os.environ["BAM_FWD_QPAIRS"] = "0"
+        o1, l1 = A.attn_forward(q, k, v, plan)
+        os.environ["BAM_FWD_QPAIRS"] = "1"
+        o2, l2 = A.attn_forward(q, k, v, plan)
+    finally:
+        if old is None:
+            os.environ.pop("BAM_FWD_QPAIRS", None)
+        else:
+            os.environ["BAM_FWD_QPAIRS"] = old
+    torch.cuda.synchronize()
+    assert (o1.float() - o2.float()).abs().max().item() < 1e-2
+    assert (l1 - l2).abs().max().item() < 1e-3
