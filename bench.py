@@ -155,6 +155,8 @@ def run_reference(args, cfg, rank, world):
 
     if rank != 0:
         return
+    # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 alone works here, on every core
+    torch.set_num_threads(max(1, len(os.sched_getaffinity(0))))
     threads = torch.get_num_threads()
     nb = sum(c for _, c in cfg["segments"]) // 128
     for w in range(args.warmup):
