@@ -22,8 +22,9 @@ def rel_l2(a, b):
     return ((a - b).norm() / b.norm()).item()
 
 
-@pytest.mark.parametrize("policy,world", [("lpt", 4), ("zigzag", 2), ("contiguous", 3)])
-def test_cp_emulated_ranks(policy, world):
+@pytest.mark.parametrize("policy,world,Hq,Hkv", [("lpt", 4, 4, 2), ("zigzag", 2, 4, 2),
+                                                 ("contiguous", 3, 4, 2), ("lpt", 3, 3, 3)])
+def test_cp_emulated_ranks(policy, world, Hq, Hkv):
     from paper_2503_11367_b200 import attention as A
     from paper_2503_11367_b200 import cp
 
@@ -31,7 +32,6 @@ def test_cp_emulated_ranks(policy, world):
     desc_l, _ = mask_ref.build_bitfield(segs)
     desc = np.asarray(desc_l, np.int64)
     T = desc.shape[0]
-    Hq, Hkv = 4, 2
     g = torch.Generator().manual_seed(1234)
     q = torch.randn(T, Hq, 128, generator=g).to(torch.bfloat16)
     k = torch.randn(T, Hkv, 128, generator=g).to(torch.bfloat16)
