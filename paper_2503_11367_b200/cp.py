@@ -176,6 +176,25 @@ class SymmExchange:
         self.kv_h = symm_mem.rendezvous(self.kv, pg.group_name)
         self.ws = symm_mem.empty((ws_n,), dtype=torch.float32, device=device)
         self.ws_h = symm_mem.rendezvous(self.ws, pg.group_name)
+        # one stream per peer so the copies run on several copy engines at once
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
+
+    def _fan_out(self, copies):
+        """Run copies[r]() on peer stream r, joined back into the current stream."""
+        cur = torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(cur)
+        done = []
+        for r, fn in enumerate(copies):
+            st = self.streams[r]
+            st.wait_event(start)
+            with torch.cuda.stream(st):
+                fn()
+            ev = torch.cuda.Event()
+            ev.record(st)
+            done.append(ev)
+        for ev in done:
+            cur.wait_event(ev)
 
     def gather(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor):
         """This rank's [n_local*128, nkv, d] K/V slice of head group gi ->
@@ -188,11 +207,17 @@ class SymmExchange:
         k_all = torch.empty((self.world * rows, nkv, d), dtype=k_g.dtype, device=k_g.device)
         v_all = torch.empty_like(k_all)
         self.kv_h.barrier(channel=0)          # every rank's slice is in place
-        for step in range(self.world):
-            r = (self.rank + step) % self.world
-            src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, self.kv_off[gi])
-            k_all[r * rows:(r + 1) * rows].copy_(src[0])
-            v_all[r * rows:(r + 1) * rows].copy_(src[1])
+
+        def pull(r):
+            def fn():
+                src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, self.kv_off[gi])
+                k_all[r * rows:(r + 1) * rows].copy_(src[0])
+                v_all[r * rows:(r + 1) * rows].copy_(src[1])
+            return fn
+        self._fan_out([pull((self.rank + step) % self.world) for step in range(self.world)])
+        for t in (k_all, v_all):
+            for st in self.streams:
+                t.record_stream(st)
         self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
         return k_all, v_all
 
@@ -202,12 +227,17 @@ class SymmExchange:
         nkv, rows, d = dk_all.shape[1], self.rows, self.d
         per = rows * nkv * d
         base = self.ws_off[gi]
-        for step in range(self.world):
-            r = (self.rank + step) % self.world
-            dst = self.ws_h.get_buffer(r, (2, rows, nkv, d), torch.float32,
-                                       base + self.rank * 2 * per)
-            dst[0].copy_(dk_all[r * rows:(r + 1) * rows])
-            dst[1].copy_(dv_all[r * rows:(r + 1) * rows])
+        def push(r):
+            def fn():
+                dst = self.ws_h.get_buffer(r, (2, rows, nkv, d), torch.float32,
+                                           base + self.rank * 2 * per)
+                dst[0].copy_(dk_all[r * rows:(r + 1) * rows])
+                dst[1].copy_(dv_all[r * rows:(r + 1) * rows])
+            return fn
+        self._fan_out([push((self.rank + step) % self.world) for step in range(self.world)])
+        for t in (dk_all, dv_all):
+            for st in self.streams:
+                t.record_stream(st)
         self.ws_h.barrier(channel=0)          # every rank's partials have landed
         red = self.ws[base:base + self.world * 2 * per].view(self.world, 2, rows, nkv, d).sum(0)
         self.ws_h.barrier(channel=0)          # summed before the next pushes
