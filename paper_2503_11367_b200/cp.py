@@ -149,6 +149,9 @@ def scatter_dkv(dk_all: torch.Tensor, dv_all: torch.Tensor, layout: CPLayout, gr
     return dk[:n], dv[:n]
 
 
+_EXCHANGES: dict = {}
+
+
 class SymmExchange:
     """Copy-engine K/V all-gather and dK/dV reduce-scatter over NVLink peer
     memory (torch symmetric memory, CUDA IPC).  Every rank's
@@ -163,7 +166,7 @@ class SymmExchange:
 
         pg = group if group is not None else dist.group.WORLD
         self.world, self.rank = layout.world, layout.rank
-        self.rows, self.d, self.n_local = layout.max_blocks * BLOCK, d, layout.n_local * BLOCK
+        self.rows, self.d = layout.max_blocks * BLOCK, d
         self.kv_off, self.ws_off = [], []
         kv_n = ws_n = 0
         for _, nkv in head_groups:
@@ -221,7 +224,7 @@ class SymmExchange:
         self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
         return k_all, v_all
 
-    def reduce_scatter(self, gi: int, dk_all: torch.Tensor, dv_all: torch.Tensor):
+    def reduce_scatter(self, gi: int, dk_all: torch.Tensor, dv_all: torch.Tensor, n_local: int):
         """fp32 partials [world*rows, nkv, d] of every key -> this rank's
         summed [n_local*128, nkv, d] dK and dV."""
         nkv, rows, d = dk_all.shape[1], self.rows, self.d
@@ -241,7 +244,7 @@ class SymmExchange:
         self.ws_h.barrier(channel=0)          # every rank's partials have landed
         red = self.ws[base:base + self.world * 2 * per].view(self.world, 2, rows, nkv, d).sum(0)
         self.ws_h.barrier(channel=0)          # summed before the next pushes
-        return red[0, :self.n_local], red[1, :self.n_local]
+        return red[0, :n_local], red[1, :n_local]
 
 
 @dataclass
@@ -250,16 +253,18 @@ class CPPlan:
     attn: A.AttentionPlan
     assignment: B.DeviceAssignment
     policy: str
-    _exchange: dict = None
 
     def exchange(self, head_groups, d, device, group=None) -> SymmExchange:
-        """The copy-engine transport for this plan (built once per head-group split)."""
-        key = (tuple(head_groups), d, str(device), id(group))
-        if self._exchange is None:
-            self._exchange = {}
-        if key not in self._exchange:
-            self._exchange[key] = SymmExchange(self.layout, head_groups, d, device, group)
-        return self._exchange[key]
+        """The copy-engine transport for this plan's shapes.  The symmetric
+        buffers depend only on (world, rank, padded rows, head groups, d), so
+        plans of the same shape (a new mask every batch) share one exchange;
+        building one is a collective, reached in the same order on every rank."""
+        key = (self.layout.world, self.layout.rank, self.layout.max_blocks, tuple(head_groups), d,
+               str(device), id(group))
+        ex = _EXCHANGES.get(key)
+        if ex is None:
+            ex = _EXCHANGES[key] = SymmExchange(self.layout, head_groups, d, device, group)
+        return ex
 
     @property
     def predicted_imbalance(self) -> float:
@@ -368,7 +373,8 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
             comm.wait_event(ev)
             dk_all.record_stream(comm)
             dv_all.record_stream(comm)
-            parts.append(ex.reduce_scatter(i, dk_all, dv_all) if ex is not None else
+            parts.append(ex.reduce_scatter(i, dk_all, dv_all, plan.layout.n_local * BLOCK)
+                         if ex is not None else
                          scatter_dkv(dk_all, dv_all, plan.layout, group))
         kv0 += nkv
     dq = ws.finalize()
