@@ -17,13 +17,21 @@
 // S_b / dP_b are double-buffered (b = step & 1), so the MMAs of step s+1's
 // S/dP run while the compute warps turn step s into P / dS, and dV/dK/dQ of
 // step s run while the compute warps work on step s+1.  dQ^T puts d on the
-// TMEM lanes, so the dQ warps' fp32 reductions into dq_acc are coalesced
-// (one 128-B row segment per warp instruction).
-// Q/dO half tiles stream through a 4-stage TMA ring.
+// TMEM lanes; the dQ warps stage each 64-query dQ^T tile (32 KB fp32) in shared
+// memory and one TMA bulk reduce-add adds it into the head-major accumulator.
+// Q/dO half tiles (+ the (lse, D) pairs) stream through a 3-stage TMA ring.
 // Warp roles (448 threads, 1 CTA / SM):
 //   warps 0-7 compute (two warpgroups, 32 query columns each; thread r = key
 //   row r), warps 8-11 dQ epilogue (thread r = head-dim column r), warp 12
 //   MMA issuer + TMEM alloc, warp 13 TMA producer (Q/dO half tiles + LSE/D).
+// CTA pairs (clusters of 2 along the slot axis) whose key blocks share one
+// step list multicast each Q/dO stage to both CTAs.
+// Bounds (profiles/r01/bwd_variants.md): shared memory feeds
+// ~288 KB per step (2250 clk at 128 B/clk against 1280 tensor clk), and the
+// fp32 dQ reduce-adds into L2 (357 GB per config-4 launch) run at ~3.6 TB/s.
+// Compile-time variants kept for the measurements there: BAM_DQ_MODE,
+// BAM_BWD_KVT, BAM_BWD_SLOT_MAJOR, BAM_BWD_POLY_EVERY, and the development
+// aids BAM_TRACE, BAM_EXPERIMENT_MMA_ONLY, BAM_EXPERIMENT_NO_DQ_RED.
 #include "../../include/bam.h"
 #include "common.cuh"
 #include "scan.cuh"
