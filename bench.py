@@ -431,7 +431,7 @@ def main():
                          "peak_source": peak_src + " " + peak_kind +
                          " (kernel timed inside a long step)",
                          "peak_burst": peak_burst, "frac_of_burst": bwd_achieved / peak_burst,
-                         "fwd": {"kernel": "bam attn_fwd_kernel", "achieved": fwd_achieved,
+                         "fwd": {"kernel": "bam attn_fwd_split_kernel (GQA head pairs)", "achieved": fwd_achieved,
                                  "frac": fwd_achieved / peak,
                                  "frac_of_burst": fwd_achieved / peak_burst}},
             "cpu_baseline": cpu_baseline,
