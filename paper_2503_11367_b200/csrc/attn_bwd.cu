@@ -7,28 +7,31 @@
 // GQA group.  A step is one 64-row half of a query block for one head
 // (j outer, head, half inner, so CTAs running together hit the same dQ
 // accumulator lines in L2):
-//   S^T  = K Q^T      (SS, M=128 keys, N=64)  -> TMEM S_b      P^T = exp2(S^T c - LSE)
-//                     (P^T bf16 of queries [32c, 32c+32) over S_b cols [32c, 32c+16),
-//                      dS^T bf16 over [32c+16, 32c+32))
-//   dP^T = V dO^T     (SS)                    -> TMEM dP_b     dS^T = P^T (dP^T - D)
-//   dV  += P^T dO     (TS: P^T bf16 in S_b, dO MN-major)       -> TMEM [0,128)
-//   dK  += dS^T Q     (TS: dS^T bf16 in TMEM S_b, Q MN-major)  -> TMEM [128,256)
-//   dQ^T = K^T dS^T   (SS: K MN-major, dS^T MN-major)          -> TMEM dP_b
-// S_b / dP_b are double-buffered (b = step & 1), so the MMAs of step s+1's
-// S/dP run while the compute warps turn step s into P / dS, and dV/dK/dQ of
-// step s run while the compute warps work on step s+1.  dQ^T puts d on the
-// TMEM lanes; the dQ warps stage each 64-query dQ^T tile (32 KB fp32) in shared
-// memory and one TMA bulk reduce-add adds it into the head-major accumulator.
-// Q/dO half tiles (+ the (lse, D) pairs) stream through a 3-stage TMA ring.
+// Default (BAM_BWD_KVT = 1): K and V are copied into TMEM once per CTA and are
+// the A operands of the TS MMAs
+//   S^T  = K Q^T      (TS, M=128 keys, N=64)  -> TMEM S        P^T = exp2(S^T c - LSE)
+//                     (P^T bf16 of queries [32c, 32c+32) over S cols [32c, 32c+16))
+//   dP^T = V dO^T     (TS)                    -> TMEM dP       dS^T = P^T (dP^T - D)
+//   dV  += P^T dO     (TS: P^T bf16 in S, dO MN-major)         -> TMEM [0,128)
+//   dK  += dS^T Q     (SS: dS^T K-major in smem, Q MN-major)   -> TMEM [128,256)
+//   dQ^T = K^T dS^T   (SS: K MN-major, dS^T MN-major)          -> TMEM dP
+// with S / dP single-buffered: S(s+1) is issued right after dV(s) so it runs
+// while the compute warps turn dP(s) into dS(s).  The all-SS variant
+// (BAM_BWD_KVT = 0) double-buffers S_b / dP_b instead (b = step & 1) and keeps
+// dS^T in TMEM for a TS dK.  dQ^T puts d on the TMEM lanes; the dQ warps stage
+// each 64-query dQ^T tile (32 KB fp32) in shared memory (two stages: the freed V
+// region and one more) and one TMA bulk reduce-add adds it into the head-major
+// accumulator.  Q/dO half tiles (+ the (lse, D) pairs) stream through a 3-stage
+// TMA ring.
 // Warp roles (448 threads, 1 CTA / SM):
 //   warps 0-7 compute (two warpgroups, 32 query columns each; thread r = key
 //   row r), warps 8-11 dQ epilogue (thread r = head-dim column r), warp 12
 //   MMA issuer + TMEM alloc, warp 13 TMA producer (Q/dO half tiles + LSE/D).
 // CTA pairs (clusters of 2 along the slot axis) whose key blocks share one
 // step list multicast each Q/dO stage to both CTAs.
-// Bounds (profiles/r01/bwd_variants.md): shared memory feeds
-// ~288 KB per step (2250 clk at 128 B/clk against 1280 tensor clk), and the
-// fp32 dQ reduce-adds into L2 (357 GB per config-4 launch) run at ~3.6 TB/s.
+// Bounds (profiles/r01/bwd_variants.md): the fp32 dQ reduce-adds
+// into L2 (357 GB per config-4 launch) run at ~3.6 TB/s device-wide; shared
+// memory feeds 128 B/clk (~224 KB per step here, 288 KB in the all-SS variant).
 // Compile-time variants kept for the measurements there: BAM_DQ_MODE,
 // BAM_BWD_KVT, BAM_BWD_SLOT_MAJOR, BAM_BWD_POLY_EVERY, and the development
 // aids BAM_TRACE, BAM_EXPERIMENT_MMA_ONLY, BAM_EXPERIMENT_NO_DQ_RED.
@@ -57,13 +60,20 @@ constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
 // of 176 KB (an SS MMA with N = 64 is shared-memory bound at 48 clk per k-step,
 // a TS one runs at the 32-clk tensor rate: tools/mma_bench.cu), at the price of
 // single-buffered S / dP, which puts the softmax / dS work on the MMA chain.
-// Measured on config 4: MMA pipeline alone 1600 vs 1240 TFLOP/s, full kernel
-// 915 vs 955 TFLOP/s, both bounded by the dQ reduce-add traffic into L2
-// (DESIGN.md "Backward bounds").  0 (default) = double-buffered, S / dP SS.
+// Measured on config 4: MMA pipeline alone 1600 vs 1240 TFLOP/s; with the dQ
+// staging double-buffered (BAM_DQ_STAGE2, so the single-buffered chain never
+// waits on a bulk reduce) the full kernel runs 1020-1038 vs 975-985 TFLOP/s.
+// 1 (default).  0 = double-buffered S / dP, both SS, one 32-KB dQ stage.
 #ifndef BAM_BWD_KVT
-#define BAM_BWD_KVT 0
+#define BAM_BWD_KVT 1
 #endif
-constexpr int kStages = (BAM_DQ_BULK && !BAM_BWD_KVT) ? 3 : 4;
+// BAM_BWD_KVT: a second 32-KB dQ staging buffer (the first is the V region), so
+// the dQ warps drain TMEM without waiting for the previous bulk reduce to read
+// its buffer (costs a Q/dO stage); the single-buffered S/dP chain needs it.
+#ifndef BAM_DQ_STAGE2
+#define BAM_DQ_STAGE2 (BAM_BWD_KVT && BAM_DQ_BULK)
+#endif
+constexpr int kStages = (BAM_DQ_BULK && (!BAM_BWD_KVT || BAM_DQ_STAGE2)) ? 3 : 4;
 // Grid order.  Slot-major (key blocks fastest, one KV head after the other):
 // the ~148 CTAs resident together are key blocks of ONE KV head, so their dQ
 // reductions land in that head group's quarter-GiB slice of dq_acc, whose
@@ -90,7 +100,7 @@ struct Smem {
   alignas(1024) uint8_t v[kTileBytes];
   alignas(1024) uint8_t ds[BAM_BWD_KVT ? 1 : 2][kDsBytes];
   Stage st[kStages];
-#if BAM_DQ_BULK && !BAM_BWD_KVT
+#if BAM_DQ_BULK && (!BAM_BWD_KVT || BAM_DQ_STAGE2)
   alignas(128) float dq_stage[64 * 128];  // dQ tile [64 queries][128 d] fp32 for the bulk reduce
 #endif
   alignas(16) float ld[kStages][128];   // per stage: (lse * log2e, delta) pairs, 64 queries
@@ -659,10 +669,11 @@ __global__ void __maxnreg__(128)
     StepIter it(col, grp, hkv, p.h_begin);
 #if BAM_DQ_BULK
 #if BAM_BWD_KVT
-    float* const dq_stage = reinterpret_cast<float*>(sm.v);  // V lives in TMEM by now
+    float* const dq_stage0 = reinterpret_cast<float*>(sm.v);  // V lives in TMEM by now
 #else
-    float* const dq_stage = sm.dq_stage;
+    float* const dq_stage0 = sm.dq_stage;
 #endif
+    int n_export = 0;
 #endif
     for (int s = 0; s < (kMmaOnly ? 0 : nsteps); ++s) {
 #if BAM_BWD_KVT
@@ -690,9 +701,16 @@ __global__ void __maxnreg__(128)
 #endif
       if (si.cls == 0) continue;  // pair step this key block skips: dQ^T is zero
 #if BAM_DQ_BULK
-      // staging buffer free once the previous bulk reduce has read it
+      // staging buffer free once the bulk reduce that last used it has read it
       const bool dq_leader = threadIdx.x == kWarpDQ * 32;
+#if BAM_BWD_KVT && BAM_DQ_STAGE2
+      float* const dq_stage = (n_export++ & 1) ? sm.dq_stage : dq_stage0;
+      if (dq_leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+#else
+      float* const dq_stage = dq_stage0;
+      (void)n_export;
       if (dq_leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
       BAM_TRACE_EV(trace_cta && dq_leader, 13, s);
       named_bar_sync(1, 128);
 #pragma unroll
