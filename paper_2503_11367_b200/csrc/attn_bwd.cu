@@ -74,6 +74,9 @@ constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
 #define BAM_DQ_STAGE2 (BAM_BWD_KVT && BAM_DQ_BULK)
 #endif
 constexpr int kStages = (BAM_DQ_BULK && (!BAM_BWD_KVT || BAM_DQ_STAGE2)) ? 3 : 4;
+#ifndef BAM_DQ_SLEEP_NS
+#define BAM_DQ_SLEEP_NS 64
+#endif
 // Grid order.  Slot-major (key blocks fastest, one KV head after the other):
 // the ~148 CTAs resident together are key blocks of ONE KV head, so their dQ
 // reductions land in that head group's quarter-GiB slice of dq_acc, whose
@@ -686,7 +689,8 @@ __global__ void __maxnreg__(128)
       const StepInfo si = it.get();
       it.next();
       float* dst = p.dq_acc + ((int64_t)si.h * Tq + si.jq * 128 + si.half * 64) * 128 + d;
-      mbar_wait_sleep(&sm.bar_dq_full[b], dq_par);
+      // on the K/V-in-TMEM chain (dP(s+1) waits for this drain): short back-off
+      mbar_wait_sleep<BAM_DQ_SLEEP_NS>(&sm.bar_dq_full[b], dq_par);
       BAM_TRACE_EV(trace_cta && threadIdx.x == kWarpDQ * 32, 8, s);
       tc_fence_after();
       uint32_t a[32], c2[32];
