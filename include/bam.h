@@ -169,7 +169,7 @@ int bam_attn_fwd_combine(const BamAttnFwdParams* p, const int32_t* combine, int3
 
 /* Backward.  dq (bf16) for the local rows; dk/dv fp32 partial gradients for
  * every key row of k/v (the contributions of the local queries; summed over
- * CP ranks by a reduce-scatter).  delta ([Hq, nq*128, 2] fp32) and dq_acc
+ * CP ranks by a reduce-scatter).  delta ([Hq, 2, nq*128] fp32) and dq_acc
  * ([nq*128, Hq, 128] fp32) are caller workspaces. */
 typedef struct BamAttnBwdParams {
   const void* q;
@@ -178,7 +178,7 @@ typedef struct BamAttnBwdParams {
   const void* o;
   const void* dout;         /* bf16 [nq*128, Hq, 128]             */
   const float* lse;         /* [Hq, nq*128] from the forward      */
-  float* delta;             /* workspace [Hq, nq*128, 2]: (lse*log2e, rowsum(dO*O)) */
+  float* delta;             /* workspace [Hq, 2, nq*128]: lse*log2e, then rowsum(dO*O) */
   float* dq_acc;            /* workspace [Hq, nq*128, 128] fp32 (head-major) */
   void* dq;                 /* bf16 [nq*128, Hq, 128] out         */
   float* dk;                /* fp32 [k_rows*128, Hkv, 128] out    */

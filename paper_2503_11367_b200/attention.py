@@ -305,7 +305,7 @@ class BackwardWorkspace:
         self.q, self.o, self.lse, self.do, self.plan = q, o, lse, do, plan
         self.scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else float(scale)
         Hq, dev = q.shape[1], q.device
-        self.delta = torch.empty(Hq, q.shape[0], 2, dtype=torch.float32, device=dev)
+        self.delta = torch.empty(Hq, 2, q.shape[0], dtype=torch.float32, device=dev)
         self.dq_acc = torch.empty(Hq, q.shape[0], 128, dtype=torch.float32, device=dev)
         self.dq = torch.empty_like(q)
         # preprocess and finalize only touch q-shaped buffers: k/v pointers unused there

@@ -169,13 +169,14 @@ constexpr bool kMmaOnly = false;
 constexpr int kBwdPoly = BAM_BWD_POLY_EVERY;
 // (The all-SS kernel runs at 128 registers and keeps the scalar forms: the
 // register pairs FFMA2 needs make it spill; its softmax is off the MMA chain.)
-__device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, const float4& v, float sc,
-                                         int i2, uint32_t allow) {
+__device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, float lse0, float lse1,
+                                         float sc, int i2, uint32_t allow) {
 #if BAM_BWD_KVT
   const float2 x = ffma2(make_float2(__uint_as_float(s0), __uint_as_float(s1)),
-                         make_float2(sc, sc), make_float2(-v.x, -v.z));
+                         make_float2(sc, sc), make_float2(-lse0, -lse1));
 #else
-  const float2 x = make_float2(fmaf(__uint_as_float(s0), sc, -v.x), fmaf(__uint_as_float(s1), sc, -v.z));
+  const float2 x = make_float2(fmaf(__uint_as_float(s0), sc, -lse0),
+                               fmaf(__uint_as_float(s1), sc, -lse1));
 #endif
   float2 p = (kBwdPoly > 0 && i2 % (kBwdPoly > 0 ? kBwdPoly : 1) == kBwdPoly - 1)
                  ? ex2_poly2(x)
@@ -185,12 +186,12 @@ __device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, const float4&
   return p;
 }
 // dS = P (dP - D) for the same pair
-__device__ __forceinline__ float2 ds_pair(float2 p, uint32_t dp0, uint32_t dp1, const float4& v) {
+__device__ __forceinline__ float2 ds_pair(float2 p, uint32_t dp0, uint32_t dp1, float D0, float D1) {
 #if BAM_BWD_KVT
   return fmul2(p, fadd2(make_float2(__uint_as_float(dp0), __uint_as_float(dp1)),
-                        make_float2(-v.y, -v.w)));
+                        make_float2(-D0, -D1)));
 #else
-  return make_float2(p.x * (__uint_as_float(dp0) - v.y), p.y * (__uint_as_float(dp1) - v.w));
+  return make_float2(p.x * (__uint_as_float(dp0) - D0), p.y * (__uint_as_float(dp1) - D1));
 #endif
 }
 
@@ -316,8 +317,10 @@ __global__ void __maxnreg__(128)
           tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0,
                         leader);
         }
-        bulk_load_w(sm.ld[st], p.delta + 2 * ((int64_t)si.h * Tq + row0), 512, &sm.bar_full[st],
+        bulk_load_w(sm.ld[st], p.delta + (int64_t)si.h * 2 * Tq + row0, 256, &sm.bar_full[st],
                     leader);
+        bulk_load_w(sm.ld[st] + 64, p.delta + (int64_t)si.h * 2 * Tq + Tq + row0, 256,
+                    &sm.bar_full[st], leader);
       }
     }
   } else if (warp == kWarpMMA) {
@@ -529,12 +532,16 @@ __global__ void __maxnreg__(128)
           allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
       }
       tmem_wait_ld();
-      const float4* ld = reinterpret_cast<const float4*>(sm.ld[st] + c * 64);  // (lse*log2e, D)
+      // this warpgroup's 32 queries: lse*log2e at ld[32c ..], D at ld[64 + 32c ..]
+      const float4* lse4 = reinterpret_cast<const float4*>(sm.ld[st] + c * 32);
+      const float4* d4 = reinterpret_cast<const float4*>(sm.ld[st] + 64 + c * 32);
       {
         uint32_t pk[16];
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
-          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], ld[i2], scale_log2, i2, allow);
+          const float4 l4 = lse4[i2 >> 1];
+          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], (i2 & 1) ? l4.z : l4.x,
+                                   (i2 & 1) ? l4.w : l4.y, scale_log2, i2, allow);
           sr[2 * i2] = __float_as_uint(pp.x);
           sr[2 * i2 + 1] = __float_as_uint(pp.y);
           pk[i2] = pack_bf16(pp.x, pp.y);
@@ -551,11 +558,14 @@ __global__ void __maxnreg__(128)
       uint32_t dr[32], dsk[16];
       BAM_TMEM_LD32(tdP + c * 32, dr);
       tmem_wait_ld();
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 16, s);
 #pragma unroll
       for (int i2 = 0; i2 < 16; ++i2) {
+        const float4 D4 = d4[i2 >> 1];
         const float2 ds = ds_pair(make_float2(__uint_as_float(sr[2 * i2]),
                                               __uint_as_float(sr[2 * i2 + 1])),
-                                  dr[2 * i2], dr[2 * i2 + 1], ld[i2]);
+                                  dr[2 * i2], dr[2 * i2 + 1], (i2 & 1) ? D4.z : D4.x,
+                                  (i2 & 1) ? D4.w : D4.y);
         dsk[i2] = pack_bf16(ds.x, ds.y);
       }
       // dS^T row r, query columns 32c .. 32c+31 (the A operand of dK, B of dQ^T)
@@ -567,7 +577,9 @@ __global__ void __maxnreg__(128)
                      "r"(dsk[q4 * 4 + 3])
                      : "memory");
       }
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 17, s);
       fence_async_smem();
+      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 18, s);
       tc_fence_before();
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 7, s);
       mbar_arrive(&sm.bar_ds_ready);
@@ -596,13 +608,16 @@ __global__ void __maxnreg__(128)
       }
       tmem_wait_ld();
       BAM_TRACE_EV(threadIdx.x == 0, 17, s);
-      const float4* ld = reinterpret_cast<const float4*>(sm.ld[st] + c * 64);  // (lse*log2e, D)
+      const float4* lse4 = reinterpret_cast<const float4*>(sm.ld[st] + c * 32);
+      const float4* d4 = reinterpret_cast<const float4*>(sm.ld[st] + 64 + c * 32);
       uint32_t pk[16], dsk[16];
 #pragma unroll
       for (int i2 = 0; i2 < 16; ++i2) {
-        const float4 v = ld[i2];
-        const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], v, scale_log2, i2, allow);
-        const float2 ds = ds_pair(pp, dr[2 * i2], dr[2 * i2 + 1], v);
+        const float4 l4 = lse4[i2 >> 1], D4 = d4[i2 >> 1];
+        const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], (i2 & 1) ? l4.z : l4.x,
+                                 (i2 & 1) ? l4.w : l4.y, scale_log2, i2, allow);
+        const float2 ds = ds_pair(pp, dr[2 * i2], dr[2 * i2 + 1], (i2 & 1) ? D4.z : D4.x,
+                                  (i2 & 1) ? D4.w : D4.y);
         pk[i2] = pack_bf16(pp.x, pp.y);
         dsk[i2] = pack_bf16(ds.x, ds.y);
       }
@@ -754,11 +769,12 @@ __global__ void __maxnreg__(128)
   }
 }
 
-// ld[h, row] = (lse[h, row] * log2e, sum_d dO[row, h, d] * O[row, h, d])  (one warp per (row, h))
+// ld[h, 0, row] = lse[h, row] * log2e, ld[h, 1, row] = sum_d dO[row, h, d] * O[row, h, d]
+// (one warp per (row, h))
 __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
                                  const __nv_bfloat16* __restrict__ dout,
                                  const float* __restrict__ lse, int64_t rows, int H,
-                                 float2* __restrict__ ld) {
+                                 float* __restrict__ ld) {
   const int64_t nw = rows * H;
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
        w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -775,7 +791,8 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
     for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
     if (lane_id() == 0) {
       const int64_t row = w / H, h = w % H;
-      ld[h * rows + row] = make_float2(lse[h * rows + row] * 1.4426950408889634f, acc);
+      ld[h * 2 * rows + row] = lse[h * rows + row] * 1.4426950408889634f;
+      ld[h * 2 * rows + rows + row] = acc;
     }
   }
 }
@@ -886,7 +903,7 @@ int bam_attn_bwd_preprocess(const BamAttnBwdParams* pp, void* stream) {
   const int64_t rows = (int64_t)p.nq * 128;
   bwd::bwd_delta_kernel<<<148 * 8, 256, 0, s>>>((const __nv_bfloat16*)p.o,
                                                 (const __nv_bfloat16*)p.dout, p.lse, rows, p.Hq,
-                                                reinterpret_cast<float2*>(p.delta));
+                                                p.delta);
   BAM_LAUNCH_CHECK();
   BAM_CUDA_TRY(cudaMemsetAsync(p.dq_acc, 0, sizeof(float) * rows * p.Hq * 128, s));
   return kOk;
