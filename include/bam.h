@@ -157,6 +157,12 @@ typedef struct BamAttnFwdParams {
   float* part_ml;
   int32_t n_items;
   int32_t pad_;
+  /* Optional CP overlap (GQA head-pair kernel): kv_ready[g] >= kv_epoch once
+   * rank g's K/V rows (block-rows [g*kv_rows_per_rank, (g+1)*kv_rows_per_rank)
+   * of k/v) have landed; tiles of other ranks wait for it, this rank's
+   * (kv_rank) do not.  kv_ready == NULL: k/v are complete at launch. */
+  const int32_t* kv_ready;
+  int32_t kv_epoch, kv_rank, kv_rows_per_rank, pad2_;
 } BamAttnFwdParams;
 int bam_attn_fwd(const BamAttnFwdParams* p, void* stream);
 
@@ -238,6 +244,11 @@ int bam_attn_fwd_2cta(const BamAttnFwdParams* p, const int32_t* pair_ids, int32_
 int bam_attn_fwd_qpairs(const BamAttnFwdParams* p, const int32_t* pair_ids, int32_t n_pairs,
                         const int32_t* slot_q, const int32_t* slot_off, const int32_t* slot_tiles,
                         void* stream);
+
+/* Stream-ordered 32-bit store (cuStreamWriteValue32, executed without an SM
+ * after the stream's prior work, with a memory barrier): the arrival flags of
+ * BamAttnFwdParams.kv_ready. */
+int bam_stream_write_i32(int32_t* dst, int32_t value, void* stream);
 
 /* ---- token permutation ----------------- */
 /* The CP runtime permutes tokens into the LPT block layout before attention

@@ -31,7 +31,8 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("items", c_vp), ("part_o", c_vp), ("part_ml", c_vp), ("n_items", c_i32),
-                ("pad_", c_i32)]
+                ("pad_", c_i32), ("kv_ready", c_vp), ("kv_epoch", c_i32), ("kv_rank", c_i32),
+                ("kv_rows_per_rank", c_i32), ("pad2_", c_i32)]
 
 
 class BamAttnBwdParams(ctypes.Structure):
@@ -70,6 +71,7 @@ SIGNATURES = {
     "bam_attn_bwd_finalize": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "bam_permute_blocks": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "bam_stream_write_i32": (c_i32, [c_vp, c_i32, c_vp]),
     "bam_attn_fwd_2cta": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp, c_i32, c_vp, c_vp, c_vp,
                                   c_vp]),
     "bam_attn_fwd_qpairs": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp, c_i32, c_vp, c_vp,

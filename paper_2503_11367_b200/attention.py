@@ -227,8 +227,14 @@ def build_split_schedule(plan: AttentionPlan, subblock: int) -> SplitSchedule:
 
 
 def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
-                 h_begin: int = 0, nh: int = 0, out=None, schedule: SplitSchedule | None = None):
+                 h_begin: int = 0, nh: int = 0, out=None, schedule: SplitSchedule | None = None,
+                 kv_ready=None):
     """Returns (o bf16 [nq*128, Hq, 128], lse fp32 [Hq, nq*128]).
+
+    ``kv_ready=(flags, epoch, rank, rows_per_rank)`` (context parallelism with
+    the copy-engine exchange): k/v may still be arriving; the GQA head-pair
+    kernel waits per tile until ``flags[owner] >= epoch`` for tiles of other
+    ranks (owner = block-row // rows_per_rank) and starts on this rank's own.
 
     Head groups (context-parallel pipelining): with ``nh`` > 0 only query
     heads [h_begin, h_begin+nh) are computed, against the ``k.shape[1]`` KV
@@ -260,6 +266,14 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         part_o.data_ptr() if part_o is not None else None,
         part_ml.data_ptr() if part_ml is not None else None,
         schedule.n_items if schedule is not None else 0, 0)
+    if kv_ready is not None:
+        if schedule is not None or (nh // Hkv) % 2:
+            raise ValueError("kv_ready needs whole rows and an even GQA group")
+        flags, epoch, rank, rows_per_rank = kv_ready
+        p.kv_ready, p.kv_epoch, p.kv_rank, p.kv_rows_per_rank = (flags.data_ptr(), int(epoch),
+                                                                 int(rank), int(rows_per_rank))
+        _lib.call("bam_attn_fwd", p)   # the head-pair kernel honours the flags
+        return o, lse
     if (schedule is None and plan.fwd_pair_ids is not None and (nh // Hkv) % 2 == 0
             and os.environ.get("BAM_FWD_2CTA", "0") == "1"):
         # shared query-block pairs on CTA pairs, the rest as whole-row items.  Opt-in:

@@ -25,6 +25,7 @@ of group g overlaps the backward kernel of group g+1.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -181,6 +182,7 @@ class SymmExchange:
         self.ws_h = symm_mem.rendezvous(self.ws, pg.group_name)
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
+        self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
 
     def _fan_out(self, copies):
         """Run copies[r]() on peer stream r, joined back into the current stream."""
@@ -198,6 +200,49 @@ class SymmExchange:
             done.append(ev)
         for ev in done:
             cur.wait_event(ev)
+
+    def gather_overlapped(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor):
+        """gather() that lets the attention start early: this rank's rows go
+        straight into the gathered buffers before the barrier (event
+        ``ev_local``), and each peer's pull is followed by a stream-ordered
+        flag store ``flags[peer] = epoch`` (bam_stream_write_i32, no SM), which
+        the forward kernel waits on per tile.  ``ev_all``: every pull landed.
+        Returns (k_all, v_all, ev_local, ev_all, (flags, epoch))."""
+        nkv, rows, d = k_g.shape[1], self.rows, self.d
+        per = rows * nkv * d
+        mine = self.kv[self.kv_off[gi]:self.kv_off[gi] + 2 * per].view(2, rows, nkv, d)
+        mine[0, :k_g.shape[0]].copy_(k_g)
+        mine[1, :v_g.shape[0]].copy_(v_g)
+        k_all = torch.empty((self.world * rows, nkv, d), dtype=k_g.dtype, device=k_g.device)
+        v_all = torch.empty_like(k_all)
+        lo = self.rank * rows
+        k_all[lo:lo + k_g.shape[0]].copy_(k_g)
+        v_all[lo:lo + v_g.shape[0]].copy_(v_g)
+        self.kv_h.barrier(channel=0)          # every rank's slice is in place
+        cur = torch.cuda.current_stream()
+        ev_local = torch.cuda.Event()
+        ev_local.record(cur)
+        if self.flags is None:
+            self.flags = torch.zeros(self.world, dtype=torch.int32, device=k_g.device)
+        self.epoch += 1
+        epoch = self.epoch
+
+        def pull(r):
+            def fn():
+                src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, self.kv_off[gi])
+                k_all[r * rows:(r + 1) * rows].copy_(src[0])
+                v_all[r * rows:(r + 1) * rows].copy_(src[1])
+                _lib.call("bam_stream_write_i32", self.flags[r:r + 1].data_ptr(), epoch)
+            return fn
+        peers = [(self.rank + step) % self.world for step in range(1, self.world)]
+        self._fan_out([pull(r) for r in peers])
+        for t in (k_all, v_all):
+            for st in self.streams:
+                t.record_stream(st)
+        ev_all = torch.cuda.Event()
+        ev_all.record(cur)
+        self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
+        return k_all, v_all, ev_local, ev_all, (self.flags, epoch)
 
     def gather(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor):
         """This rank's [n_local*128, nkv, d] K/V slice of head group gi ->
@@ -285,7 +330,25 @@ def make_cp_plan(mask_or_desc, world: int, rank: int, policy: str = "lpt") -> CP
     layout = cp_layout(asg.owner, world, rank)
     attn = A.build_plan(desc, q_gid=layout.local_blocks, k_row=layout.k_row,
                         k_rows=world * layout.max_blocks, classes=classes, W=W)
+    _local_tiles_first(attn, layout)
     return CPPlan(layout=layout, attn=attn, assignment=asg, policy=policy)
+
+
+def _local_tiles_first(attn: A.AttentionPlan, layout: CPLayout) -> None:
+    """Reorder every query row's key tiles so that the tiles of keys this rank
+    owns come first (stable otherwise): with the copy-engine exchange the
+    forward works on them while the peers' K/V are still being pulled.  The
+    online softmax does not depend on the tile order; the backward's column
+    lists and the query-pair union lists are separate arrays."""
+    n = int(attn.row_off[-1].item())
+    if n == 0 or layout.world == 1:
+        return
+    rt = attn.row_tiles[:n]
+    remote = (layout.owner.to(torch.int64)[(rt >> 2).to(torch.int64)] != layout.rank)
+    counts = (attn.row_off[1:] - attn.row_off[:-1]).to(torch.int64)
+    row = torch.repeat_interleave(torch.arange(counts.shape[0], device=rt.device), counts)
+    order = torch.sort(row * 2 + remote.to(torch.int64), stable=True).indices
+    attn.row_tiles[:n] = rt[order]
 
 
 _COMM_STREAMS: dict = {}
@@ -327,6 +390,20 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     gathered, events = [], []
     hg = _head_groups(Hkv, groups)
     ex = plan.exchange(hg, k_loc.shape[2], k_loc.device, group) if transport == "ce" else None
+    if (ex is not None and len(hg) == 1 and grp % 2 == 0
+            and os.environ.get("BAM_CP_OVERLAP", "1") != "0"):
+        # the forward starts on this rank's key tiles while the copy engines pull the
+        # peers' K/V; its tiles of other ranks wait on per-rank arrival flags
+        comm.wait_stream(cur)
+        with torch.cuda.stream(comm):
+            k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(0, k_loc, v_loc)
+        cur.wait_event(ev_local)
+        k_all.record_stream(cur)
+        v_all.record_stream(cur)
+        A.attn_forward(q_loc, k_all, v_all, plan.attn, scale, out=(o, lse),
+                       kv_ready=(flags, epoch, plan.layout.rank, plan.layout.max_blocks))
+        cur.wait_event(ev_all)
+        return o, lse, [(k_all, v_all)]
     comm.wait_stream(cur)
     with torch.cuda.stream(comm):
         for gi, (kv0, nkv) in enumerate(hg):

@@ -640,9 +640,20 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i], 0, hh[i], jj[i] * 128, leader);
         tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i] + kTileBytes / 2, 64, hh[i], jj[i] * 128, leader);
       }
+      uint64_t ready = 0;  // CP overlap: ranks whose K/V rows are known to have landed
       for (int t = 0; t < n; ++t) {
         const int st = t & 1;
-        const int krow = p.k_row[tiles[t] >> 2] * 128;
+        const int kblk = p.k_row[tiles[t] >> 2];
+        const int krow = kblk * 128;
+        if (p.kv_ready) {
+          const int owner = kblk / p.kv_rows_per_rank;
+          if (owner != p.kv_rank && !((ready >> owner) & 1)) {
+            if (lane == 0) wait_flag_geq(p.kv_ready + owner, p.kv_epoch);
+            __syncwarp();
+            fence_proxy_async_global();  // the copy engine's data before the TMA reads
+            ready |= 1ull << owner;
+          }
+        }
         if (t >= 2) mbar_wait_sleep(&sm.bar_k_empty[st], ((t >> 1) - 1) & 1);
         mbar_expect_tx_w(&sm.bar_k_full[st], kTileBytes, leader);
         tma_load_3d_w(&tm_k, &sm.bar_k_full[st], sm.k[st], 0, hkv, krow, leader);

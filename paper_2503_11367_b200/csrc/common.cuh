@@ -168,6 +168,20 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+// Spin (with back-off, bounded) until *flag >= value, acquire at GPU scope.
+__device__ __forceinline__ void wait_flag_geq(const int32_t* flag, int32_t value) {
+  uint32_t iters = 0;
+  while (true) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= value) break;
+    __nanosleep(128);
+    if (++iters > (1u << 26)) mbar_timeout_trap();
+  }
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma reads)
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

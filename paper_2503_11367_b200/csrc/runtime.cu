@@ -152,3 +152,30 @@ int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
 }
 
 }  // extern "C"
+
+// Stream-ordered flag store (cuStreamWriteValue32 through the runtime's driver
+// entry point, so libbam needs no -lcuda): no SM involved, ordered after the
+// stream's previous work with a memory barrier.
+extern "C" int bam_stream_write_i32(int32_t* dst, int32_t value, void* stream) {
+  using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &ptr, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      bam::set_last_error("cuStreamWriteValue32 unavailable from the driver");
+      return bam::kCudaError;
+    }
+    fn = reinterpret_cast<Fn>(ptr);
+  }
+  BAM_CHECK_ARG(dst != nullptr && (reinterpret_cast<uintptr_t>(dst) & 3) == 0,
+                "bam_stream_write_i32: bad destination");
+  const CUresult r = fn((CUstream)stream, (CUdeviceptr)dst, (cuuint32_t)value, 0);
+  if (r != CUDA_SUCCESS) {
+    bam::set_last_error("cuStreamWriteValue32 failed (%d)", (int)r);
+    return bam::kCudaError;
+  }
+  return bam::kOk;
+}
