@@ -139,6 +139,7 @@ KERNELS_PER_CALL = {
     "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
     "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
     "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1,
+    "bam_stream_write_i32": 0,   # a stream memory operation, not a kernel
 }
 launch_count = 0
 
