@@ -391,14 +391,16 @@ __global__ void __maxnreg__(128)
         BAM_XWAIT(&sm.bar_ds_ready, ph);
         BAM_TRACE_EV(trace_cta && leader, 14, s);
         tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q  (A = dS^T K-major in shared memory)
-          mma_ss_w(tmem + kColDK, d_ds0 + 2 * kk, dqmn + kk * 128, id_kv, (s > 0 || kk > 0),
-                   leader);
+        // dQ^T first and committed on its own: the dQ warps drain it (and dP(s+1),
+        // which reuses its columns, can start) while dK(s) runs
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T -> the dP columns
           mma_ss_w(tDP, dk_kmn + kk * 128, d_ds0 + kk * 128, id_q, kk > 0, leader);
         tc_commit_w(&sm.bar_dq_full[0], leader);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q  (A = dS^T K-major in shared memory)
+          mma_ss_w(tmem + kColDK, d_ds0 + 2 * kk, dqmn + kk * 128, id_kv, (s > 0 || kk > 0),
+                   leader);
         if (shared)
           tc_commit_mc_w(&sm.bar_empty[st], 0x3, leader);
         else
