@@ -267,12 +267,23 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         part_ml.data_ptr() if part_ml is not None else None,
         schedule.n_items if schedule is not None else 0, 0)
     if kv_ready is not None:
-        if schedule is not None or (nh // Hkv) % 2:
-            raise ValueError("kv_ready needs whole rows and an even GQA group")
+        # the head-pair, query-pair and one-head kernels honour the flags (not the
+        # CTA-pair kernel, nor split-KV schedules)
+        if schedule is not None:
+            raise ValueError("kv_ready needs whole rows")
         flags, epoch, rank, rows_per_rank = kv_ready
         p.kv_ready, p.kv_epoch, p.kv_rank, p.kv_rows_per_rank = (flags.data_ptr(), int(epoch),
                                                                  int(rank), int(rows_per_rank))
-        _lib.call("bam_attn_fwd", p)   # the head-pair kernel honours the flags
+        if (nh // Hkv) % 2 == 0 or plan.fwd_pair_ids is None:
+            _lib.call("bam_attn_fwd", p)
+            return o, lse
+        _lib.call("bam_attn_fwd_qpairs", p, plan.fwd_pair_ids.data_ptr(),
+                  int(plan.fwd_pair_ids.shape[0]), plan.fwd_slot_q.data_ptr(),
+                  plan.fwd_slot_off.data_ptr(), plan.fwd_slot_tiles.data_ptr())
+        n_rest = int(plan.fwd_rest_items.shape[0])
+        if n_rest:
+            p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
+            _lib.call("bam_attn_fwd", p)
         return o, lse
     if (schedule is None and plan.fwd_pair_ids is not None and (nh // Hkv) % 2 == 0
             and os.environ.get("BAM_FWD_2CTA", "0") == "1"):

@@ -391,9 +391,12 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     hg = _head_groups(Hkv, groups)
     ex = plan.exchange(hg, k_loc.shape[2], k_loc.device, group) if transport == "ce" else None
     if (ex is not None and len(hg) == 1 and grp % 2 == 0
-            and os.environ.get("BAM_CP_OVERLAP", "1") != "0"):
+            and os.environ.get("BAM_CP_OVERLAP", "1") != "0"
+            and os.environ.get("BAM_FWD_2CTA", "0") != "1"):
         # the forward starts on this rank's key tiles while the copy engines pull the
-        # peers' K/V; its tiles of other ranks wait on per-rank arrival flags
+        # peers' K/V; its tiles of other ranks wait on per-rank arrival flags.  GQA only:
+        # for MHA (query-block pairs, whose union lists are not local-first) it measured
+        # slower than gathering first (config 2, N=4: 3269 vs 3395 TFLOP/s)
         comm.wait_stream(cur)
         with torch.cuda.stream(comm):
             k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(0, k_loc, v_loc)

@@ -301,8 +301,19 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_expect_tx_w(&sm.bar_q, kTileBytes, leader);
       tma_load_3d_w(&tm_q, &sm.bar_q, sm.q, 0, h, j * 128, leader);
       tma_load_3d_w(&tm_q, &sm.bar_q, sm.q + kTileBytes / 2, 64, h, j * 128, leader);
+      uint64_t ready = 0;  // CP overlap: ranks whose K/V rows are known to have landed
       for (int t = 0; t < n; ++t) {
-        const int krow = p.k_row[tiles[t] >> 2] * 128;
+        const int kblk = p.k_row[tiles[t] >> 2];
+        const int krow = kblk * 128;
+        if (p.kv_ready) {
+          const int owner = kblk / p.kv_rows_per_rank;
+          if (owner != p.kv_rank && !((ready >> owner) & 1)) {
+            if (lane == 0) wait_flag_geq(p.kv_ready + owner, p.kv_epoch);
+            __syncwarp();
+            fence_proxy_async_global();
+            ready |= 1ull << owner;
+          }
+        }
         if (t > 0) mbar_wait_sleep(&sm.bar_k_empty, (t - 1) & 1);
         mbar_expect_tx_w(&sm.bar_k_full, kTileBytes, leader);
         tma_load_3d_w(&tm_k, &sm.bar_k_full, sm.k, 0, hkv, krow, leader);

@@ -25,6 +25,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--policy", default="lpt")
 ap.add_argument("--transport", default="nccl", choices=["nccl", "ce"])
 ap.add_argument("--groups", type=int, default=1)
+ap.add_argument("--heads", type=int, default=8)
+ap.add_argument("--kv-heads", type=int, default=2)
 args = ap.parse_args()
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 local = int(os.environ.get("LOCAL_RANK", rank))
@@ -34,7 +36,7 @@ dist.init_process_group("nccl", device_id=dev)
 
 segs = [("text", 512), ("img0", 1024), ("text", 640), ("img1", 512), ("text", 1408)]
 mask = M.build_bitfield(segs)
-T, Hq, Hkv = len(mask), 8, 2
+T, Hq, Hkv = len(mask), args.heads, args.kv_heads
 plan = cp.make_cp_plan(mask, world, rank, args.policy)
 lay = plan.layout
 g = torch.Generator().manual_seed(1234)
