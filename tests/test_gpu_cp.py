@@ -189,3 +189,37 @@ def test_cp_single_rank_transports_match_local(transport):
     for name, a, b in zip(("O", "dQ", "dK", "dV"), *outs):
         assert (a.float() - b.float()).abs().max().item() < 1e-2, name
     assert torch.equal(outs[0][0], outs[1][0])
+
+
+def test_forward_waits_on_kv_arrival_flags():
+    """The overlapped CP forward: the head-pair kernel starts while half of
+    the key blocks (a 'peer' rank's rows) are still being copied on another
+    stream, and waits per tile on the arrival flag that bam_stream_write_i32
+    sets after the copy.  Must equal the forward on complete K/V."""
+    from paper_2503_11367_b200 import _lib
+    from paper_2503_11367_b200 import attention as A
+    from paper_2503_11367_b200 import mask as M
+
+    mask = M.build_bitfield([("text", 512), ("img0", 512), ("text", 512), ("img1", 512)])
+    nb, T, Hq, Hkv = len(mask) // BLOCK, len(mask), 8, 2
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(9)
+    q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    plan = A.plan_for_mask(mask)                 # k_row = identity: "rank r" owns rows r*nb/2..
+    o_ref, lse_ref = A.attn_forward(q, k, v, plan)
+    half = nb // 2 * BLOCK
+    k2, v2 = torch.zeros_like(k), torch.zeros_like(v)
+    k2[:half], v2[:half] = k[:half], v[:half]    # rank 0 (this rank): present at launch
+    flags = torch.zeros(2, dtype=torch.int32, device=dev)
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(50_000_000)            # the peer's rows land well after the launch
+        k2[half:].copy_(k[half:])
+        v2[half:].copy_(v[half:])
+        _lib.call("bam_stream_write_i32", flags[1:2].data_ptr(), 7)
+    o, lse = A.attn_forward(q, k2, v2, plan, kv_ready=(flags, 7, 0, nb // 2))
+    torch.cuda.synchronize()
+    assert torch.equal(o, o_ref) and torch.equal(lse, lse_ref)
