@@ -205,6 +205,13 @@ typedef struct BamAttnBwdParams {
    * tile to both CTAs (each loads one half). */
   const int32_t* pair_shared;
   int32_t n_slots, pad_;
+  /* Optional CP reduce-scatter overlap: head_done[hkv] is incremented (after a
+   * GPU-scope fence) by every CTA of KV head hkv when it has written its dK/dV
+   * rows, so a stream waiting for head_done[h] >= CTAs per head (grid.x) can
+   * ship head h while the kernel still runs.  dkv_head_major != 0: dk / dv are
+   * [Hkv, k_rows*128, 128] (each head's partials contiguous). */
+  int32_t* head_done;
+  int32_t dkv_head_major, pad2_;
 } BamAttnBwdParams;
 int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
 /* The three launches bam_attn_bwd performs, exposed for per-kernel timing:
@@ -249,6 +256,9 @@ int bam_attn_fwd_qpairs(const BamAttnFwdParams* p, const int32_t* pair_ids, int3
  * after the stream's prior work, with a memory barrier): the arrival flags of
  * BamAttnFwdParams.kv_ready. */
 int bam_stream_write_i32(int32_t* dst, int32_t value, void* stream);
+/* Stream-ordered wait (cuStreamWaitValue32, GEQ): the stream's later work
+ * starts once *src >= value (the backward's head_done counters). */
+int bam_stream_wait_i32_geq(const int32_t* src, int32_t value, void* stream);
 
 /* ---- token permutation ----------------- */
 /* The CP runtime permutes tokens into the LPT block layout before attention

@@ -42,7 +42,8 @@ class BamAttnBwdParams(ctypes.Structure):
                 ("col_off", c_vp), ("col_tiles", c_vp), ("order", c_vp),
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
-                ("pair_shared", c_vp), ("n_slots", c_i32), ("pad_", c_i32)]
+                ("pair_shared", c_vp), ("n_slots", c_i32), ("pad_", c_i32),
+                ("head_done", c_vp), ("dkv_head_major", c_i32), ("pad2_", c_i32)]
 
 
 # name -> (restype, argtypes); mirrors include/bam.h exactly
@@ -72,6 +73,7 @@ SIGNATURES = {
     "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "bam_permute_blocks": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "bam_stream_write_i32": (c_i32, [c_vp, c_i32, c_vp]),
+    "bam_stream_wait_i32_geq": (c_i32, [c_vp, c_i32, c_vp]),
     "bam_attn_fwd_2cta": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp, c_i32, c_vp, c_vp, c_vp,
                                   c_vp]),
     "bam_attn_fwd_qpairs": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp, c_i32, c_vp, c_vp,
@@ -139,7 +141,7 @@ KERNELS_PER_CALL = {
     "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
     "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
     "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1,
-    "bam_stream_write_i32": 0,   # a stream memory operation, not a kernel
+    "bam_stream_write_i32": 0, "bam_stream_wait_i32_geq": 0,   # stream memory operations
 }
 launch_count = 0
 

@@ -336,9 +336,16 @@ class BackwardWorkspace:
         # preprocess and finalize only touch q-shaped buffers: k/v pointers unused there
         self._call("bam_attn_bwd_preprocess", q, q, q, q, 0, 0, 1)
 
-    def _params(self, k, v, dk, dv, h_begin, nh, Hkv):
+    def _pairs(self) -> bool:
+        return self.plan.pair_shared is not None and os.environ.get("BAM_BWD_PAIRS", "1") != "0"
+
+    def ctas_per_head(self) -> int:
+        """CTAs of the main kernel per KV head (what head_done[h] counts up to)."""
+        return int(self.plan.slot_kb.shape[0]) if self._pairs() else self.plan.nb
+
+    def _params(self, k, v, dk, dv, h_begin, nh, Hkv, head_done=None, head_major=False):
         pl = self.plan
-        pairs = pl.pair_shared is not None and os.environ.get("BAM_BWD_PAIRS", "1") != "0"
+        pairs = self._pairs()
         col_off, col_tiles, order = ((pl.slot_off, pl.slot_tiles, pl.slot_kb) if pairs else
                                      (pl.col_off, pl.col_tiles, pl.bwd_order))
         return _lib.BamAttnBwdParams(
@@ -349,22 +356,27 @@ class BackwardWorkspace:
             col_tiles.data_ptr(), order.data_ptr(), pl.nq, pl.nb, pl.k_rows,
             self.q.shape[1], Hkv, self.scale, h_begin, nh,
             pl.pair_shared.data_ptr() if pairs else None,
-            int(pl.slot_kb.shape[0]) if pairs else 0, 0)
+            int(pl.slot_kb.shape[0]) if pairs else 0, 0,
+            head_done.data_ptr() if head_done is not None else None, int(head_major), 0)
 
-    def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv):
-        _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv))
+    def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv, **kw):
+        _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv, **kw))
 
-    def main(self, k, v, *, h_begin=0, nh=0, timer=None):
-        """dK/dV fp32 partials [k_rows*128, Hkv, 128] of the head group; dQ accumulates."""
+    def main(self, k, v, *, h_begin=0, nh=0, timer=None, head_done=None, head_major=False):
+        """dK/dV fp32 partials of the head group, [k_rows*128, Hkv, 128] (or
+        [Hkv, k_rows*128, 128] with head_major); dQ accumulates.  head_done
+        (int32 [Hkv], zeroed): per-KV-head CTA completion counters."""
         Hkv = k.shape[1]
         nh = _check_group(self.q.shape[1], Hkv, h_begin, nh)
         if k.shape != v.shape or k.shape[0] != self.plan.k_rows * BLOCK or not k.is_contiguous():
             raise ValueError(f"k/v must be contiguous [{self.plan.k_rows * BLOCK}, Hkv, 128]")
-        dk = torch.empty(k.shape, dtype=torch.float32, device=k.device)
-        dv = torch.empty(k.shape, dtype=torch.float32, device=k.device)
+        shape = (Hkv, k.shape[0], k.shape[2]) if head_major else k.shape
+        dk = torch.empty(shape, dtype=torch.float32, device=k.device)
+        dv = torch.empty(shape, dtype=torch.float32, device=k.device)
         if timer is not None:
             timer[0].record()
-        self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv)
+        self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv, head_done=head_done,
+                   head_major=head_major)
         if timer is not None:
             timer[1].record()
         return dk, dv

@@ -269,6 +269,36 @@ class SymmExchange:
         self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
         return k_all, v_all
 
+    def reduce_scatter_heads(self, dk_all, dv_all, n_local: int, head_done, ctas_per_head: int):
+        """reduce_scatter() for head-major partials [Hkv, world*rows, d] of one
+        head group that the backward kernel is STILL WRITING: every peer stream
+        waits (cuStreamWaitValue32, no SM) until head h's CTAs are done, then
+        pushes head h, so the transfer of heads 0..Hkv-2 overlaps the kernel.
+        Call with the current stream just before the kernel's launch point
+        ordered (the streams wait on an event recorded now)."""
+        Hkv, rows, d = dk_all.shape[0], self.rows, self.d
+        per = rows * Hkv * d
+        base = self.ws_off[0]
+
+        def push(r):
+            def fn():
+                dst = self.ws_h.get_buffer(r, (2, Hkv, rows, d), torch.float32,
+                                           base + self.rank * 2 * per)
+                for h in range(Hkv):
+                    _lib.call("bam_stream_wait_i32_geq", head_done[h:h + 1].data_ptr(),
+                              ctas_per_head)
+                    dst[0, h].copy_(dk_all[h, r * rows:(r + 1) * rows])
+                    dst[1, h].copy_(dv_all[h, r * rows:(r + 1) * rows])
+            return fn
+        self._fan_out([push((self.rank + step) % self.world) for step in range(self.world)])
+        for t in (dk_all, dv_all, head_done):
+            for st in self.streams:
+                t.record_stream(st)
+        self.ws_h.barrier(channel=0)          # every rank's partials have landed
+        red = self.ws[base:base + self.world * 2 * per].view(self.world, 2, Hkv, rows, d).sum(0)
+        self.ws_h.barrier(channel=0)          # summed before the next pushes
+        return (red[0, :, :n_local].transpose(0, 1), red[1, :, :n_local].transpose(0, 1))
+
     def reduce_scatter(self, gi: int, dk_all: torch.Tensor, dv_all: torch.Tensor, n_local: int):
         """fp32 partials [world*rows, nkv, d] of every key -> this rank's
         summed [n_local*128, nkv, d] dK and dV."""
@@ -442,6 +472,24 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
     hg = [(sum(k.shape[1] for k, _ in gathered[:i]), k.shape[1]) for i, (k, _) in
           enumerate(gathered)]
     ex = plan.exchange(hg, q_loc.shape[2], q_loc.device, group) if transport == "ce" else None
+    if (ex is not None and len(gathered) == 1
+            and os.environ.get("BAM_CP_RS_OVERLAP", "1") != "0"):
+        # the copy engines ship each KV head's dK/dV partials as soon as the
+        # backward kernel's CTAs of that head have finished (per-head counters)
+        k_all, v_all = gathered[0]
+        head_done = torch.zeros(k_all.shape[1], dtype=torch.int32, device=q_loc.device)
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        dk_all, dv_all = ws.main(k_all, v_all, head_done=head_done, head_major=True,
+                                 timer=None if timers is None else timers[0])
+        with torch.cuda.stream(comm):
+            comm.wait_event(ready)
+            head_done.record_stream(comm)
+            dk, dv = ex.reduce_scatter_heads(dk_all, dv_all, plan.layout.n_local * BLOCK,
+                                             head_done, ws.ctas_per_head())
+        dq = ws.finalize()
+        cur.wait_stream(comm)
+        return dq, A.to_bf16(dk.contiguous()), A.to_bf16(dv.contiguous())
     parts, kv0 = [], 0
     for i, (k_all, v_all) in enumerate(gathered):
         nkv = k_all.shape[1]

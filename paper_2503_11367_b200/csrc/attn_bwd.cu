@@ -652,7 +652,9 @@ __global__ void __maxnreg__(128)
     if (kb < 0) goto done;  // padding slot of the last cluster
     {
     const int64_t row = (int64_t)krow0 + r;
-    float* dst = (c == 0 ? p.dv : p.dk) + (row * p.Hkv + hkv) * 128;
+    float* dst = (c == 0 ? p.dv : p.dk) +
+                 (p.dkv_head_major ? ((int64_t)hkv * p.k_rows * 128 + row) * 128
+                                   : (row * p.Hkv + hkv) * 128);
     const float mul = c == 0 ? 1.f : p.scale;
     if (nsteps > 0) {
 #if BAM_BWD_KVT
@@ -764,6 +766,10 @@ __global__ void __maxnreg__(128)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.head_done != nullptr && threadIdx.x == 0) {  // this CTA's dK/dV rows are written
+    __threadfence();
+    atomicAdd(p.head_done + hkv, 1);
+  }
   if (cluster_mode) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == kWarpMMA) {
     tc_fence_after();

@@ -179,3 +179,28 @@ extern "C" int bam_stream_write_i32(int32_t* dst, int32_t value, void* stream) {
   }
   return bam::kOk;
 }
+
+extern "C" int bam_stream_wait_i32_geq(const int32_t* src, int32_t value, void* stream) {
+  using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &ptr, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      bam::set_last_error("cuStreamWaitValue32 unavailable from the driver");
+      return bam::kCudaError;
+    }
+    fn = reinterpret_cast<Fn>(ptr);
+  }
+  BAM_CHECK_ARG(src != nullptr && (reinterpret_cast<uintptr_t>(src) & 3) == 0,
+                "bam_stream_wait_i32_geq: bad source");
+  const CUresult r = fn((CUstream)stream, (CUdeviceptr)src, (cuuint32_t)value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) {
+    bam::set_last_error("cuStreamWaitValue32 failed (%d)", (int)r);
+    return bam::kCudaError;
+  }
+  return bam::kOk;
+}
