@@ -273,6 +273,18 @@ int bam_permute_blocks(const void* const* src, void* const* dst, const int64_t* 
                        int32_t n_tensors, const int32_t* idx, int32_t n_blocks,
                        int32_t block_rows, int32_t scatter, void* stream);
 
+/* Sum of n_parts fp32 partials -> bf16, the tail of the dK/dV reduce-scatter
+ * (every rank's partials land in this rank's symmetric workspace):
+ *   dst_c[row, h, 0:128] = bf16(sum_p src[p*part_stride + c*comp_stride +
+ *                                        h*head_stride + row*row_stride + 0:128])
+ * for row < n_rows, h < n_heads, c = 0 (dst0) and, when dst1 != NULL, c = 1
+ * (dst1).  Outputs are token-major [n_rows, n_heads, 128] bf16; strides are
+ * in floats; head dim 128, 16-byte aligned pointers and strides. */
+int bam_reduce_partials_bf16(const float* src, int32_t n_parts, int64_t part_stride,
+                             int64_t comp_stride, int64_t head_stride, int64_t row_stride,
+                             int32_t n_heads, int64_t n_rows, void* dst0, void* dst1,
+                             void* stream);
+
 /* fp32 -> bf16 conversion (dk/dv partials to the bf16 gradient layout). */
 int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
 

@@ -71,6 +71,8 @@ SIGNATURES = {
     "bam_attn_bwd_main": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_attn_bwd_finalize": (c_i32, [ctypes.POINTER(BamAttnBwdParams), c_vp]),
     "bam_f32_to_bf16": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
+    "bam_reduce_partials_bf16": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i64, c_i32, c_i64,
+                                         c_vp, c_vp, c_vp]),
     "bam_permute_blocks": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "bam_stream_write_i32": (c_i32, [c_vp, c_i32, c_vp]),
     "bam_stream_wait_i32_geq": (c_i32, [c_vp, c_i32, c_vp]),
@@ -140,6 +142,7 @@ KERNELS_PER_CALL = {
     "bam_contiguous_assign": 1, "bam_split_count": 2, "bam_split_fill": 1,
     "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
     "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
+    "bam_reduce_partials_bf16": 1,
     "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1,
     "bam_stream_write_i32": 0, "bam_stream_wait_i32_geq": 0,   # stream memory operations
 }

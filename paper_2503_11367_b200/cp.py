@@ -295,9 +295,19 @@ class SymmExchange:
             for st in self.streams:
                 t.record_stream(st)
         self.ws_h.barrier(channel=0)          # every rank's partials have landed
-        red = self.ws[base:base + self.world * 2 * per].view(self.world, 2, Hkv, rows, d).sum(0)
+        out = self._reduce(base, n_local, Hkv, part=2 * per, comp=per, head=rows * d, row=d)
         self.ws_h.barrier(channel=0)          # summed before the next pushes
-        return (red[0, :, :n_local].transpose(0, 1), red[1, :, :n_local].transpose(0, 1))
+        return out
+
+    def _reduce(self, base, n_local, nkv, *, part, comp, head, row):
+        """bf16 [n_local, nkv, d] dK and dV = sum of the world partials in the
+        workspace (one bam_reduce_partials_bf16 launch)."""
+        dk = torch.empty((n_local, nkv, self.d), dtype=torch.bfloat16, device=self.ws.device)
+        dv = torch.empty_like(dk)
+        src = self.ws[base:base + self.world * part]
+        _lib.call("bam_reduce_partials_bf16", src.data_ptr(), self.world, part, comp, head, row,
+                  nkv, n_local, dk.data_ptr(), dv.data_ptr())
+        return dk, dv
 
     def reduce_scatter(self, gi: int, dk_all: torch.Tensor, dv_all: torch.Tensor, n_local: int):
         """fp32 partials [world*rows, nkv, d] of every key -> this rank's
@@ -317,9 +327,9 @@ class SymmExchange:
             for st in self.streams:
                 t.record_stream(st)
         self.ws_h.barrier(channel=0)          # every rank's partials have landed
-        red = self.ws[base:base + self.world * 2 * per].view(self.world, 2, rows, nkv, d).sum(0)
+        out = self._reduce(base, n_local, nkv, part=2 * per, comp=per, head=d, row=nkv * d)
         self.ws_h.barrier(channel=0)          # summed before the next pushes
-        return red[0, :n_local], red[1, :n_local]
+        return out
 
 
 @dataclass
@@ -489,7 +499,9 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
                                              head_done, ws.ctas_per_head())
         dq = ws.finalize()
         cur.wait_stream(comm)
-        return dq, A.to_bf16(dk.contiguous()), A.to_bf16(dv.contiguous())
+        dk.record_stream(cur)          # allocated on the comm stream
+        dv.record_stream(cur)
+        return dq, dk, dv
     parts, kv0 = [], 0
     for i, (k_all, v_all) in enumerate(gathered):
         nkv = k_all.shape[1]
@@ -507,9 +519,13 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
         kv0 += nkv
     dq = ws.finalize()
     cur.wait_stream(comm)
+    for t in (t for pr in parts for t in pr):
+        t.record_stream(cur)           # allocated on the comm stream
     dk = torch.cat([p[0] for p in parts], dim=1) if len(parts) > 1 else parts[0][0]
     dv = torch.cat([p[1] for p in parts], dim=1) if len(parts) > 1 else parts[0][1]
-    return dq, A.to_bf16(dk.contiguous()), A.to_bf16(dv.contiguous())
+    if dk.dtype != torch.bfloat16:   # NCCL reduce-scatter: fp32 sums
+        dk, dv = A.to_bf16(dk.contiguous()), A.to_bf16(dv.contiguous())
+    return dq, dk, dv
 
 
 class _CPAttention(torch.autograd.Function):

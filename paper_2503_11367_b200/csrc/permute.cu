@@ -45,6 +45,40 @@ __global__ void __launch_bounds__(256) permute_kernel(const PermuteArgs a,
   }
 }
 
+// dst_c[row, h, 0:128] = bf16( sum_p src[p*part_stride + c*comp_stride +
+//                                       h*head_stride + row*row_stride + 0:128] )
+// One thread per 8 outputs (two float4 loads per part, one 16-B store); the
+// output order is token-major so stores are fully coalesced, and every read
+// is a whole 32-B sector run of 512 B per (row, head).
+__global__ void __launch_bounds__(256) reduce_partials_kernel(
+    const float* __restrict__ src, int32_t n_parts, int64_t part_stride, int64_t comp_stride,
+    int64_t head_stride, int64_t row_stride, int32_t n_heads, int64_t n_rows,
+    uint4* __restrict__ dst0, uint4* __restrict__ dst1, int32_t n_comp) {
+  const int64_t per_comp = n_rows * n_heads * 16;
+  const int64_t total = per_comp * n_comp;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / per_comp, r = e - c * per_comp;
+    const int64_t v = r & 15, rh = r >> 4;
+    const int64_t row = rh / n_heads, h = rh - row * n_heads;
+    const float* p = src + c * comp_stride + h * head_stride + row * row_stride + v * 8;
+    float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+    float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+    for (int q = 1; q < n_parts; ++q) {
+      const float4* pq = reinterpret_cast<const float4*>(p + q * part_stride);
+      const float4 x = __ldcs(pq), y = __ldcs(pq + 1);
+      a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+      b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+    }
+    uint4 o;
+    o.x = pack_bf16(a.x, a.y);
+    o.y = pack_bf16(a.z, a.w);
+    o.z = pack_bf16(b.x, b.y);
+    o.w = pack_bf16(b.z, b.w);
+    (c == 0 ? dst0 : dst1)[r] = o;
+  }
+}
+
 }  // namespace perm
 }  // namespace bam
 
@@ -74,6 +108,27 @@ extern "C" int bam_permute_blocks(const void* const* src, void* const* dst,
     a.total[t] = a.row_vec[t] * block_rows * (int64_t)n_blocks;
   }
   perm::permute_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(a, idx, block_rows, scatter);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+extern "C" int bam_reduce_partials_bf16(const float* src, int32_t n_parts, int64_t part_stride,
+                                        int64_t comp_stride, int64_t head_stride,
+                                        int64_t row_stride, int32_t n_heads, int64_t n_rows,
+                                        void* dst0, void* dst1, void* stream) {
+  BAM_CHECK_ARG(src && dst0 && n_parts >= 1 && n_heads >= 1 && n_rows >= 0,
+                "bam_reduce_partials_bf16: n_parts=%d n_heads=%d n_rows=%lld", n_parts, n_heads,
+                (long long)n_rows);
+  BAM_CHECK_ARG((reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(dst0) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(dst1) & 15) == 0 &&
+                    part_stride % 4 == 0 && comp_stride % 4 == 0 && head_stride % 4 == 0 &&
+                    row_stride % 4 == 0,
+                "bam_reduce_partials_bf16: pointers and strides must be 16-byte aligned");
+  if (n_rows == 0) return kOk;
+  perm::reduce_partials_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      src, n_parts, part_stride, comp_stride, head_stride, row_stride, n_heads, n_rows,
+      static_cast<uint4*>(dst0), static_cast<uint4*>(dst1), dst1 ? 2 : 1);
   BAM_LAUNCH_CHECK();
   return kOk;
 }

@@ -152,6 +152,34 @@ def test_permute_blocks_gather_scatter_bit_exact():
         cp.shard_rows(bad, lay)
 
 
+@pytest.mark.parametrize("head_major", [False, True])
+def test_reduce_partials_bf16_bit_exact(head_major):
+    """dK/dV reduce-scatter tail (bam_reduce_partials_bf16): the sum of the world
+    partials in order, rounded to bf16, for both workspace layouts, bit-exact
+    against sequential fp32 adds + torch's bf16 rounding; padded rows dropped."""
+    from paper_2503_11367_b200 import _lib
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(11)
+    world, nkv, rows, n_local, d = 3, 5, 3 * BLOCK, 2 * BLOCK + 64, 128
+    shape = (world, 2, nkv, rows, d) if head_major else (world, 2, rows, nkv, d)
+    ws = torch.randn(shape, device=dev, generator=g) * 100
+    acc = ws[0].clone()
+    for p in range(1, world):
+        acc = acc + ws[p]
+    if head_major:
+        acc = acc.transpose(1, 2)          # [2, rows, nkv, d]
+    ref = acc[:, :n_local].to(torch.bfloat16)
+    dk = torch.empty((n_local, nkv, d), dtype=torch.bfloat16, device=dev)
+    dv = torch.empty_like(dk)
+    per = rows * nkv * d
+    head, row = (rows * d, d) if head_major else (d, nkv * d)
+    _lib.call("bam_reduce_partials_bf16", ws.data_ptr(), world, 2 * per, per, head, row, nkv,
+              n_local, dk.data_ptr(), dv.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(dk, ref[0]) and torch.equal(dv, ref[1])
+
+
 @pytest.mark.parametrize("transport", ["nccl", "ce"])
 def test_cp_single_rank_transports_match_local(transport):
     """cp_bitfield_attention on a one-rank NCCL process group, through both
