@@ -160,9 +160,12 @@ typedef struct BamAttnFwdParams {
   /* Optional CP overlap (GQA head-pair kernel): kv_ready[g] >= kv_epoch once
    * rank g's K/V rows (block-rows [g*kv_rows_per_rank, (g+1)*kv_rows_per_rank)
    * of k/v) have landed; tiles of other ranks wait for it, this rank's
-   * (kv_rank) do not.  kv_ready == NULL: k/v are complete at launch. */
+   * (kv_rank) do not.  kv_ready == NULL: k/v are complete at launch.
+   * kv_head_major != 0: k and v are head-major [Hkv, k_rows*128, 128] (the
+   * copy-engine gather moves one contiguous chunk per (rank, KV head)), and
+   * kv_ready holds one flag per (rank, KV head): kv_ready[g*Hkv + hkv]. */
   const int32_t* kv_ready;
-  int32_t kv_epoch, kv_rank, kv_rows_per_rank, pad2_;
+  int32_t kv_epoch, kv_rank, kv_rows_per_rank, kv_head_major;
 } BamAttnFwdParams;
 int bam_attn_fwd(const BamAttnFwdParams* p, void* stream);
 
@@ -211,7 +214,8 @@ typedef struct BamAttnBwdParams {
    * ship head h while the kernel still runs.  dkv_head_major != 0: dk / dv are
    * [Hkv, k_rows*128, 128] (each head's partials contiguous). */
   int32_t* head_done;
-  int32_t dkv_head_major, pad2_;
+  int32_t dkv_head_major;
+  int32_t kv_head_major;    /* k/v head-major [Hkv, k_rows*128, 128] */
 } BamAttnBwdParams;
 int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
 /* The three launches bam_attn_bwd performs, exposed for per-kernel timing:

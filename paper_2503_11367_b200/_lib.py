@@ -32,7 +32,7 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("items", c_vp), ("part_o", c_vp), ("part_ml", c_vp), ("n_items", c_i32),
                 ("pad_", c_i32), ("kv_ready", c_vp), ("kv_epoch", c_i32), ("kv_rank", c_i32),
-                ("kv_rows_per_rank", c_i32), ("pad2_", c_i32)]
+                ("kv_rows_per_rank", c_i32), ("kv_head_major", c_i32)]
 
 
 class BamAttnBwdParams(ctypes.Structure):
@@ -43,7 +43,7 @@ class BamAttnBwdParams(ctypes.Structure):
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("pair_shared", c_vp), ("n_slots", c_i32), ("pad_", c_i32),
-                ("head_done", c_vp), ("dkv_head_major", c_i32), ("pad2_", c_i32)]
+                ("head_done", c_vp), ("dkv_head_major", c_i32), ("kv_head_major", c_i32)]
 
 
 # name -> (restype, argtypes); mirrors include/bam.h exactly

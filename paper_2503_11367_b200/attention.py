@@ -168,6 +168,16 @@ def _check_qkv(q, k, v, plan: AttentionPlan):
         raise ValueError("Hq must be a multiple of Hkv")
 
 
+def _check_kv_head_major(k, v, plan: AttentionPlan):
+    """Head-major K/V [Hkv, k_rows*128, 128] (the copy-engine CP gather's layout)."""
+    for name, t in (("k", k), ("v", v)):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor")
+    if k.shape != v.shape or k.dim() != 3 or k.shape[1:] != (plan.k_rows * BLOCK, HEAD_DIM):
+        raise ValueError(f"head-major k/v must be [Hkv, {plan.k_rows * BLOCK}, {HEAD_DIM}]")
+    return k.shape[0]
+
+
 def _check_group(Hq, Hkv, h_begin, nh):
     nh = nh or Hq
     if h_begin < 0 or h_begin + nh > Hq or nh % Hkv:
@@ -228,8 +238,11 @@ def build_split_schedule(plan: AttentionPlan, subblock: int) -> SplitSchedule:
 
 def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
                  h_begin: int = 0, nh: int = 0, out=None, schedule: SplitSchedule | None = None,
-                 kv_ready=None):
+                 kv_ready=None, kv_head_major: bool = False):
     """Returns (o bf16 [nq*128, Hq, 128], lse fp32 [Hq, nq*128]).
+
+    ``kv_head_major``: k/v are [Hkv, k_rows*128, 128] instead of token-major
+    (then ``kv_ready`` flags are per (rank, KV head): ``flags[owner*Hkv + hkv]``).
 
     ``kv_ready=(flags, epoch, rank, rows_per_rank)`` (context parallelism with
     the copy-engine exchange): k/v may still be arriving; the GQA head-pair
@@ -240,7 +253,11 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
     heads [h_begin, h_begin+nh) are computed, against the ``k.shape[1]`` KV
     heads of ``k``/``v``; ``out=(o, lse)`` receives them in place."""
     Hq, Hkv = q.shape[1], k.shape[1]
-    if nh or h_begin:
+    if kv_head_major:
+        Hkv = _check_kv_head_major(k, v, plan)
+        if q.dtype != torch.bfloat16 or not q.is_cuda or not q.is_contiguous():
+            raise ValueError("q must be a contiguous bf16 CUDA tensor")
+    elif nh or h_begin:
         for name, t in (("q", q), ("k", k), ("v", v)):
             if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor")
@@ -266,6 +283,7 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         part_o.data_ptr() if part_o is not None else None,
         part_ml.data_ptr() if part_ml is not None else None,
         schedule.n_items if schedule is not None else 0, 0)
+    p.kv_head_major = int(kv_head_major)
     if kv_ready is not None:
         # the head-pair, query-pair and one-head kernels honour the flags (not the
         # CTA-pair kernel, nor split-KV schedules)
@@ -343,7 +361,8 @@ class BackwardWorkspace:
         """CTAs of the main kernel per KV head (what head_done[h] counts up to)."""
         return int(self.plan.slot_kb.shape[0]) if self._pairs() else self.plan.nb
 
-    def _params(self, k, v, dk, dv, h_begin, nh, Hkv, head_done=None, head_major=False):
+    def _params(self, k, v, dk, dv, h_begin, nh, Hkv, head_done=None, head_major=False,
+                kv_head_major=False):
         pl = self.plan
         pairs = self._pairs()
         col_off, col_tiles, order = ((pl.slot_off, pl.slot_tiles, pl.slot_kb) if pairs else
@@ -357,26 +376,33 @@ class BackwardWorkspace:
             self.q.shape[1], Hkv, self.scale, h_begin, nh,
             pl.pair_shared.data_ptr() if pairs else None,
             int(pl.slot_kb.shape[0]) if pairs else 0, 0,
-            head_done.data_ptr() if head_done is not None else None, int(head_major), 0)
+            head_done.data_ptr() if head_done is not None else None, int(head_major),
+            int(kv_head_major))
 
     def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv, **kw):
         _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv, **kw))
 
-    def main(self, k, v, *, h_begin=0, nh=0, timer=None, head_done=None, head_major=False):
+    def main(self, k, v, *, h_begin=0, nh=0, timer=None, head_done=None, head_major=False,
+             kv_head_major=False):
         """dK/dV fp32 partials of the head group, [k_rows*128, Hkv, 128] (or
         [Hkv, k_rows*128, 128] with head_major); dQ accumulates.  head_done
-        (int32 [Hkv], zeroed): per-KV-head CTA completion counters."""
-        Hkv = k.shape[1]
+        (int32 [Hkv], zeroed): per-KV-head CTA completion counters.
+        kv_head_major: k/v are [Hkv, k_rows*128, 128]."""
+        rows = self.plan.k_rows * BLOCK
+        if kv_head_major:
+            Hkv = _check_kv_head_major(k, v, self.plan)
+        else:
+            Hkv = k.shape[1]
+            if k.shape != v.shape or k.shape[0] != rows or not k.is_contiguous():
+                raise ValueError(f"k/v must be contiguous [{rows}, Hkv, 128]")
         nh = _check_group(self.q.shape[1], Hkv, h_begin, nh)
-        if k.shape != v.shape or k.shape[0] != self.plan.k_rows * BLOCK or not k.is_contiguous():
-            raise ValueError(f"k/v must be contiguous [{self.plan.k_rows * BLOCK}, Hkv, 128]")
-        shape = (Hkv, k.shape[0], k.shape[2]) if head_major else k.shape
+        shape = (Hkv, rows, HEAD_DIM) if head_major else (rows, Hkv, HEAD_DIM)
         dk = torch.empty(shape, dtype=torch.float32, device=k.device)
         dv = torch.empty(shape, dtype=torch.float32, device=k.device)
         if timer is not None:
             timer[0].record()
         self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv, head_done=head_done,
-                   head_major=head_major)
+                   head_major=head_major, kv_head_major=kv_head_major)
         if timer is not None:
             timer[1].record()
         return dk, dv

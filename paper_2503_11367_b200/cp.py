@@ -201,13 +201,59 @@ class SymmExchange:
         for ev in done:
             cur.wait_event(ev)
 
-    def gather_overlapped(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor):
-        """gather() that lets the attention start early: this rank's rows go
-        straight into the gathered buffers before the barrier (event
-        ``ev_local``), and each peer's pull is followed by a stream-ordered
-        flag store ``flags[peer] = epoch`` (bam_stream_write_i32, no SM), which
-        the forward kernel waits on per tile.  ``ev_all``: every pull landed.
+    def gather_overlapped(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor,
+                          head_major: bool = True):
+        """gather() that lets the attention start early, into HEAD-MAJOR
+        buffers [nkv, world*rows, d]: this rank's rows go straight into the
+        gathered buffers before the barrier (event ``ev_local``); the peers'
+        shards are pulled one KV head at a time (one contiguous chunk per
+        (peer, head)), each followed by a stream-ordered flag store
+        ``flags[peer*nkv + h] = epoch`` (bam_stream_write_i32, no SM) that the
+        forward kernel waits on per tile, so the first heads' tiles start
+        after 1/nkv of the transfer.  ``ev_all``: every pull landed.
+        head_major=False: token-major buffers, one chunk and flag per peer.
         Returns (k_all, v_all, ev_local, ev_all, (flags, epoch))."""
+        nkv, rows, d = k_g.shape[1], self.rows, self.d
+        n = k_g.shape[0]
+        per = rows * nkv * d
+        if not head_major:
+            return self._gather_overlapped_token_major(gi, k_g, v_g)
+        mine = self.kv[self.kv_off[gi]:self.kv_off[gi] + 2 * per].view(2, nkv, rows, d)
+        mine[0, :, :n].copy_(k_g.transpose(0, 1))
+        mine[1, :, :n].copy_(v_g.transpose(0, 1))
+        k_all = torch.empty((nkv, self.world * rows, d), dtype=k_g.dtype, device=k_g.device)
+        v_all = torch.empty_like(k_all)
+        lo = self.rank * rows
+        k_all[:, lo:lo + n].copy_(mine[0, :, :n])
+        v_all[:, lo:lo + n].copy_(mine[1, :, :n])
+        self.kv_h.barrier(channel=0)          # every rank's slice is in place
+        cur = torch.cuda.current_stream()
+        ev_local = torch.cuda.Event()
+        ev_local.record(cur)
+        if self.flags is None or self.flags.numel() < self.world * nkv:
+            self.flags = torch.zeros(self.world * nkv, dtype=torch.int32, device=k_g.device)
+        self.epoch += 1
+        epoch = self.epoch
+
+        def pull(r):
+            def fn():
+                src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, self.kv_off[gi])
+                for h in range(nkv):
+                    k_all[h, r * rows:(r + 1) * rows].copy_(src[0, h])
+                    v_all[h, r * rows:(r + 1) * rows].copy_(src[1, h])
+                    _lib.call("bam_stream_write_i32", self.flags[r * nkv + h:].data_ptr(), epoch)
+            return fn
+        peers = [(self.rank + step) % self.world for step in range(1, self.world)]
+        self._fan_out([pull(r) for r in peers])
+        for t in (k_all, v_all):
+            for st in self.streams:
+                t.record_stream(st)
+        ev_all = torch.cuda.Event()
+        ev_all.record(cur)
+        self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
+        return k_all, v_all, ev_local, ev_all, (self.flags, epoch)
+
+    def _gather_overlapped_token_major(self, gi, k_g, v_g):
         nkv, rows, d = k_g.shape[1], self.rows, self.d
         per = rows * nkv * d
         mine = self.kv[self.kv_off[gi]:self.kv_off[gi] + 2 * per].view(2, rows, nkv, d)
@@ -218,11 +264,11 @@ class SymmExchange:
         lo = self.rank * rows
         k_all[lo:lo + k_g.shape[0]].copy_(k_g)
         v_all[lo:lo + v_g.shape[0]].copy_(v_g)
-        self.kv_h.barrier(channel=0)          # every rank's slice is in place
+        self.kv_h.barrier(channel=0)
         cur = torch.cuda.current_stream()
         ev_local = torch.cuda.Event()
         ev_local.record(cur)
-        if self.flags is None:
+        if self.flags is None or self.flags.numel() < self.world:
             self.flags = torch.zeros(self.world, dtype=torch.int32, device=k_g.device)
         self.epoch += 1
         epoch = self.epoch
@@ -232,16 +278,15 @@ class SymmExchange:
                 src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, self.kv_off[gi])
                 k_all[r * rows:(r + 1) * rows].copy_(src[0])
                 v_all[r * rows:(r + 1) * rows].copy_(src[1])
-                _lib.call("bam_stream_write_i32", self.flags[r:r + 1].data_ptr(), epoch)
+                _lib.call("bam_stream_write_i32", self.flags[r:].data_ptr(), epoch)
             return fn
-        peers = [(self.rank + step) % self.world for step in range(1, self.world)]
-        self._fan_out([pull(r) for r in peers])
+        self._fan_out([pull((self.rank + s) % self.world) for s in range(1, self.world)])
         for t in (k_all, v_all):
             for st in self.streams:
                 t.record_stream(st)
         ev_all = torch.cuda.Event()
         ev_all.record(cur)
-        self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
+        self.kv_h.barrier(channel=0)
         return k_all, v_all, ev_local, ev_all, (self.flags, epoch)
 
     def gather(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor):
@@ -418,7 +463,9 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     g starts as soon as its K/V have landed, overlapping the gather of group
     g+1 (the paper overlaps communication per head).
     transport "nccl": NCCL all_gather; "ce": copy-engine pulls from symmetric
-    memory (SymmExchange).  Returns (o, lse, [(k_all_g, v_all_g)])."""
+    memory (SymmExchange).  Returns (o, lse, [(k_all_g, v_all_g)]); the
+    copy-engine overlap path's single group is head-major [Hkv, rows, d]
+    (``_kv_head_major`` tells the layouts apart)."""
     if transport not in TRANSPORTS:
         raise ValueError(f"transport must be one of {TRANSPORTS}")
     Hq, Hkv = q_loc.shape[1], k_loc.shape[1]
@@ -437,14 +484,17 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
         # peers' K/V; its tiles of other ranks wait on per-rank arrival flags.  GQA only:
         # for MHA (query-block pairs, whose union lists are not local-first) it measured
         # slower than gathering first (config 2, N=4: 3269 vs 3395 TFLOP/s)
+        head_major = os.environ.get("BAM_CP_KV_HEAD_MAJOR", "1") != "0"
         comm.wait_stream(cur)
         with torch.cuda.stream(comm):
-            k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(0, k_loc, v_loc)
+            k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(
+                0, k_loc, v_loc, head_major)
         cur.wait_event(ev_local)
         k_all.record_stream(cur)
         v_all.record_stream(cur)
         A.attn_forward(q_loc, k_all, v_all, plan.attn, scale, out=(o, lse),
-                       kv_ready=(flags, epoch, plan.layout.rank, plan.layout.max_blocks))
+                       kv_ready=(flags, epoch, plan.layout.rank, plan.layout.max_blocks),
+                       kv_head_major=head_major)
         cur.wait_event(ev_all)
         return o, lse, [(k_all, v_all)]
     comm.wait_stream(cur)
@@ -469,28 +519,43 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     return o, lse, gathered
 
 
+def _kv_head_major(k_all, plan: CPPlan) -> bool:
+    """Gathered K/V are token-major [k_rows*128, nkv, d] or head-major
+    [nkv, k_rows*128, d]; nkv < 128 <= k_rows*128 tells them apart."""
+    return k_all.shape[0] != plan.attn.k_rows * BLOCK
+
+
 def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=None,
                 timers=None, transport: str = "nccl"):
     """Per KV-head group: backward kernel -> fp32 dK/dV partials of every key,
     reduce-scattered on the side stream while the next group computes."""
     Hq = q_loc.shape[1]
-    Hkv = sum(k.shape[1] for k, _ in gathered)
+    kvh = [_kv_head_major(k, plan) for k, _ in gathered]
+    if any(kvh) and len(gathered) != 1:
+        raise ValueError("head-major gathered K/V come as one head group")
+    Hkv = sum(k.shape[0] if h else k.shape[1] for (k, _), h in zip(gathered, kvh))
     grp = Hq // Hkv
     cur = torch.cuda.current_stream()
     comm = _comm_stream(q_loc.device)
     ws = A.BackwardWorkspace(q_loc, o, lse, do, plan.attn, scale)
-    hg = [(sum(k.shape[1] for k, _ in gathered[:i]), k.shape[1]) for i, (k, _) in
-          enumerate(gathered)]
+    if kvh[0]:
+        hg = [(0, Hkv)]
+    else:
+        hg = [(sum(k.shape[1] for k, _ in gathered[:i]), k.shape[1]) for i, (k, _) in
+              enumerate(gathered)]
     ex = plan.exchange(hg, q_loc.shape[2], q_loc.device, group) if transport == "ce" else None
+    if kvh[0] and ex is None:
+        raise ValueError("head-major gathered K/V need the copy-engine transport")
     if (ex is not None and len(gathered) == 1
-            and os.environ.get("BAM_CP_RS_OVERLAP", "1") != "0"):
+            and (kvh[0] or os.environ.get("BAM_CP_RS_OVERLAP", "1") != "0")):
         # the copy engines ship each KV head's dK/dV partials as soon as the
         # backward kernel's CTAs of that head have finished (per-head counters)
         k_all, v_all = gathered[0]
-        head_done = torch.zeros(k_all.shape[1], dtype=torch.int32, device=q_loc.device)
+        head_done = torch.zeros(Hkv, dtype=torch.int32, device=q_loc.device)
         ready = torch.cuda.Event()
         ready.record(cur)
         dk_all, dv_all = ws.main(k_all, v_all, head_done=head_done, head_major=True,
+                                 kv_head_major=kvh[0],
                                  timer=None if timers is None else timers[0])
         with torch.cuda.stream(comm):
             comm.wait_event(ready)

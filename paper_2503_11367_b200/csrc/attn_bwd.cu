@@ -925,8 +925,12 @@ int bam_attn_bwd_main(const BamAttnBwdParams* pp, void* stream) {
   int rc;
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, rows, p.Hq, 64))) return rc;
   if ((rc = make_tmap_rows_heads_d128(&mdo, p.dout, rows, p.Hq, 64))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128,
+                                      p.kv_head_major)))
+    return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128,
+                                      p.kv_head_major)))
+    return rc;
   const int smem = (int)sizeof(bwd::Smem);
   BAM_CUDA_TRY(cudaFuncSetAttribute(bwd::attn_bwd_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -308,7 +308,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (p.kv_ready) {
           const int owner = kblk / p.kv_rows_per_rank;
           if (owner != p.kv_rank && !((ready >> owner) & 1)) {
-            if (lane == 0) wait_flag_geq(p.kv_ready + owner, p.kv_epoch);
+            if (lane == 0)
+              wait_flag_geq(p.kv_ready + (p.kv_head_major ? owner * p.Hkv + hkv : owner),
+                            p.kv_epoch);
             __syncwarp();
             fence_proxy_async_global();
             ready |= 1ull << owner;
@@ -659,7 +661,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         if (p.kv_ready) {
           const int owner = kblk / p.kv_rows_per_rank;
           if (owner != p.kv_rank && !((ready >> owner) & 1)) {
-            if (lane == 0) wait_flag_geq(p.kv_ready + owner, p.kv_epoch);
+            if (lane == 0)
+              wait_flag_geq(p.kv_ready + (p.kv_head_major ? owner * p.Hkv + hkv : owner),
+                            p.kv_epoch);
             __syncwarp();
             fence_proxy_async_global();  // the copy engine's data before the TMA reads
             ready |= 1ull << owner;
@@ -992,8 +996,12 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
   CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128,
+                                      p.kv_head_major)))
+    return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128,
+                                      p.kv_head_major)))
+    return rc;
   const int grp = nh / p.Hkv;
   if (grp % 2 == 0) {  // GQA head pairs, split-row softmax
     const int smem = (int)sizeof(fwd::SplitSmem);
@@ -1030,8 +1038,12 @@ extern "C" int bam_attn_fwd_2cta(const BamAttnFwdParams* pp, const int32_t* pair
   CUtensorMap mq, mk64, mv;
   int rc;
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mk64, p.k, (int64_t)p.k_rows * 128, p.Hkv, 64))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mk64, p.k, (int64_t)p.k_rows * 128, p.Hkv, 64,
+                                      p.kv_head_major)))
+    return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128,
+                                      p.kv_head_major)))
+    return rc;
   const int smem = (int)sizeof(fwd::Pair2Smem);
   BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_2cta_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1069,8 +1081,12 @@ extern "C" int bam_attn_fwd_qpairs(const BamAttnFwdParams* pp, const int32_t* pa
   CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
-  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128))) return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mk, p.k, (int64_t)p.k_rows * 128, p.Hkv, 128,
+                                      p.kv_head_major)))
+    return rc;
+  if ((rc = make_tmap_rows_heads_d128(&mv, p.v, (int64_t)p.k_rows * 128, p.Hkv, 128,
+                                      p.kv_head_major)))
+    return rc;
   const int smem = (int)sizeof(fwd::SplitSmem);
   BAM_CUDA_TRY(cudaFuncSetAttribute(fwd::attn_fwd_split_kernel<true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -25,7 +25,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int make_tmap_rows_heads_d128(CUtensorMap* map, const void* base, int64_t rows, int heads,
-                              int box_rows) {
+                              int box_rows, bool head_major) {
   auto encode = get_encode();
   if (!encode) {
     set_last_error("cuTensorMapEncodeTiled unavailable from the driver");
@@ -37,6 +37,10 @@ int make_tmap_rows_heads_d128(CUtensorMap* map, const void* base, int64_t rows, 
   }
   cuuint64_t dims[3] = {128, (cuuint64_t)heads, (cuuint64_t)rows};
   cuuint64_t strides[2] = {128 * 2, (cuuint64_t)heads * 128 * 2};
+  if (head_major) {
+    strides[0] = (cuuint64_t)rows * 128 * 2;
+    strides[1] = 128 * 2;
+  }
   cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,

@@ -259,3 +259,34 @@ def test_fwd_query_block_pairs_match_one_head_kernel():
     torch.cuda.synchronize()
     assert (o1.float() - o2.float()).abs().max().item() < 1e-2
     assert (l1 - l2).abs().max().item() < 1e-3
+
+
+@pytest.mark.parametrize("Hq,Hkv", [(8, 2), (4, 4)])
+def test_head_major_kv_matches_token_major(Hq, Hkv):
+    """Head-major K/V [Hkv, T, 128] (the copy-engine CP gather's layout; only
+    the TMA strides change) give bit-identical O, LSE, dK, dV to token-major
+    K/V, for the GQA head-pair and the MHA query-pair / one-head kernels; the
+    head-major dK/dV partial layout is the same numbers transposed."""
+    from paper_2503_11367_b200 import attention as A, mask as M
+
+    mask = M.build_bitfield([("text", 128), ("image", 1024), ("text", 2944)])
+    plan = A.plan_for_mask(mask)
+    T, dev = len(mask), torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(5)
+    q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    do = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    kh, vh = k.transpose(0, 1).contiguous(), v.transpose(0, 1).contiguous()
+    o, lse = A.attn_forward(q, k, v, plan)
+    oh, lseh = A.attn_forward(q, kh, vh, plan, kv_head_major=True)
+    assert torch.equal(o, oh) and torch.equal(lse, lseh)
+    ws = A.BackwardWorkspace(q, o, lse, do, plan, None)
+    dk, dv = ws.main(k, v)
+    ws.finalize()
+    wsh = A.BackwardWorkspace(q, o, lse, do, plan, None)
+    dkh, dvh = wsh.main(kh, vh, kv_head_major=True, head_major=True)
+    wsh.finalize()
+    assert torch.equal(dk, dkh.transpose(0, 1)) and torch.equal(dv, dvh.transpose(0, 1))
+    with pytest.raises(ValueError, match="head-major"):
+        A.attn_forward(q, k, v, plan, kv_head_major=True)
