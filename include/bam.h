@@ -216,6 +216,14 @@ typedef struct BamAttnBwdParams {
   int32_t* head_done;
   int32_t dkv_head_major;
   int32_t kv_head_major;    /* k/v head-major [Hkv, k_rows*128, 128] */
+  /* Optional CP reduce-scatter fused into the epilogue: when dkv_peers != NULL
+   * (a DEVICE array of one pointer per rank, each the UVA address of this
+   * rank's slot [2][Hkv][dkv_rows_per_owner][128] fp32 in that rank's
+   * symmetric workspace), the dK/dV partial rows of key row r go straight to
+   * dkv_peers[r / dkv_rows_per_owner] (dK at [0], dV at [1]; over NVLink for
+   * other ranks) and dk / dv are not written. */
+  float* const* dkv_peers;
+  int32_t dkv_rows_per_owner, pad3_;
 } BamAttnBwdParams;
 int bam_attn_bwd(const BamAttnBwdParams* p, void* stream);
 /* The three launches bam_attn_bwd performs, exposed for per-kernel timing:

@@ -362,7 +362,7 @@ class BackwardWorkspace:
         return int(self.plan.slot_kb.shape[0]) if self._pairs() else self.plan.nb
 
     def _params(self, k, v, dk, dv, h_begin, nh, Hkv, head_done=None, head_major=False,
-                kv_head_major=False):
+                kv_head_major=False, dkv_peers=None, rows_per_owner=0):
         pl = self.plan
         pairs = self._pairs()
         col_off, col_tiles, order = ((pl.slot_off, pl.slot_tiles, pl.slot_kb) if pairs else
@@ -370,24 +370,29 @@ class BackwardWorkspace:
         return _lib.BamAttnBwdParams(
             self.q.data_ptr(), k.data_ptr(), v.data_ptr(), self.o.data_ptr(), self.do.data_ptr(),
             self.lse.data_ptr(), self.delta.data_ptr(), self.dq_acc.data_ptr(),
-            self.dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), pl.desc.data_ptr(),
+            self.dq.data_ptr(), dk.data_ptr() if dk is not None else None,
+            dv.data_ptr() if dv is not None else None, pl.desc.data_ptr(),
             pl.q_gid.data_ptr(), pl.k_row.data_ptr(), col_off.data_ptr(),
             col_tiles.data_ptr(), order.data_ptr(), pl.nq, pl.nb, pl.k_rows,
             self.q.shape[1], Hkv, self.scale, h_begin, nh,
             pl.pair_shared.data_ptr() if pairs else None,
             int(pl.slot_kb.shape[0]) if pairs else 0, 0,
             head_done.data_ptr() if head_done is not None else None, int(head_major),
-            int(kv_head_major))
+            int(kv_head_major), dkv_peers.data_ptr() if dkv_peers is not None else None,
+            int(rows_per_owner), 0)
 
     def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv, **kw):
         _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv, **kw))
 
     def main(self, k, v, *, h_begin=0, nh=0, timer=None, head_done=None, head_major=False,
-             kv_head_major=False):
+             kv_head_major=False, dkv_peers=None, rows_per_owner=0):
         """dK/dV fp32 partials of the head group, [k_rows*128, Hkv, 128] (or
         [Hkv, k_rows*128, 128] with head_major); dQ accumulates.  head_done
         (int32 [Hkv], zeroed): per-KV-head CTA completion counters.
-        kv_head_major: k/v are [Hkv, k_rows*128, 128]."""
+        kv_head_major: k/v are [Hkv, k_rows*128, 128].  dkv_peers (int64 device
+        tensor of per-rank workspace-slot addresses) with rows_per_owner: the
+        partials go straight to their owners (fused reduce-scatter); returns
+        (None, None)."""
         rows = self.plan.k_rows * BLOCK
         if kv_head_major:
             Hkv = _check_kv_head_major(k, v, self.plan)
@@ -396,13 +401,17 @@ class BackwardWorkspace:
             if k.shape != v.shape or k.shape[0] != rows or not k.is_contiguous():
                 raise ValueError(f"k/v must be contiguous [{rows}, Hkv, 128]")
         nh = _check_group(self.q.shape[1], Hkv, h_begin, nh)
-        shape = (Hkv, rows, HEAD_DIM) if head_major else (rows, Hkv, HEAD_DIM)
-        dk = torch.empty(shape, dtype=torch.float32, device=k.device)
-        dv = torch.empty(shape, dtype=torch.float32, device=k.device)
+        if dkv_peers is not None:
+            dk = dv = None
+        else:
+            shape = (Hkv, rows, HEAD_DIM) if head_major else (rows, Hkv, HEAD_DIM)
+            dk = torch.empty(shape, dtype=torch.float32, device=k.device)
+            dv = torch.empty(shape, dtype=torch.float32, device=k.device)
         if timer is not None:
             timer[0].record()
         self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv, head_done=head_done,
-                   head_major=head_major, kv_head_major=kv_head_major)
+                   head_major=head_major, kv_head_major=kv_head_major, dkv_peers=dkv_peers,
+                   rows_per_owner=rows_per_owner)
         if timer is not None:
             timer[1].record()
         return dk, dv

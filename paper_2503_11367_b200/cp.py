@@ -183,6 +183,7 @@ class SymmExchange:
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
         self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
+        self._cache = {}
 
     def _fan_out(self, copies):
         """Run copies[r]() on peer stream r, joined back into the current stream."""
@@ -313,6 +314,31 @@ class SymmExchange:
                 t.record_stream(st)
         self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
         return k_all, v_all
+
+    def peer_slots(self, nkv: int) -> torch.Tensor:
+        """int64 device tensor: for every rank r, the UVA address of THIS rank's
+        slot [2][nkv][rows][d] fp32 in rank r's workspace (head group 0), which
+        the backward kernel's epilogue stores into directly (dkv_peers)."""
+        key = ("slots", nkv)
+        t = self._cache.get(key)
+        if t is None:
+            per = self.rows * nkv * self.d
+            base = self.ws_off[0] + self.rank * 2 * per
+            ptrs = [self.ws_h.get_buffer(r, (2 * per,), torch.float32, base).data_ptr()
+                    for r in range(self.world)]
+            t = self._cache[key] = torch.tensor(ptrs, dtype=torch.int64, device=self.ws.device)
+        return t
+
+    def reduce_direct(self, nkv: int, n_local: int):
+        """Tail of the fused reduce-scatter: once every rank's backward kernel has
+        stored its partials into the owners' workspaces (barrier), sum them into
+        this rank's bf16 dK/dV."""
+        per = self.rows * nkv * self.d
+        self.ws_h.barrier(channel=0)          # every rank's kernel has finished its stores
+        out = self._reduce(self.ws_off[0], n_local, nkv, part=2 * per, comp=per,
+                           head=self.rows * self.d, row=self.d)
+        self.ws_h.barrier(channel=0)          # summed before the next kernel stores
+        return out
 
     def reduce_scatter_heads(self, dk_all, dv_all, n_local: int, head_done, ctas_per_head: int):
         """reduce_scatter() for head-major partials [Hkv, world*rows, d] of one
@@ -546,6 +572,24 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
     ex = plan.exchange(hg, q_loc.shape[2], q_loc.device, group) if transport == "ce" else None
     if kvh[0] and ex is None:
         raise ValueError("head-major gathered K/V need the copy-engine transport")
+    if (ex is not None and len(gathered) == 1
+            and os.environ.get("BAM_CP_RS_DIRECT", "1") != "0"):
+        # reduce-scatter fused into the backward epilogue: each CTA stores its fp32
+        # dK/dV partial rows straight into the key owner's symmetric workspace
+        # (NVLink stores); after the kernel only a barrier and the local sum remain
+        k_all, v_all = gathered[0]
+        ws.main(k_all, v_all, kv_head_major=kvh[0], dkv_peers=ex.peer_slots(Hkv),
+                rows_per_owner=ex.rows, timer=None if timers is None else timers[0])
+        done = torch.cuda.Event()
+        done.record(cur)
+        with torch.cuda.stream(comm):
+            comm.wait_event(done)
+            dk, dv = ex.reduce_direct(Hkv, plan.layout.n_local * BLOCK)
+        dq = ws.finalize()
+        cur.wait_stream(comm)
+        dk.record_stream(cur)          # allocated on the comm stream
+        dv.record_stream(cur)
+        return dq, dk, dv
     if (ex is not None and len(gathered) == 1
             and (kvh[0] or os.environ.get("BAM_CP_RS_OVERLAP", "1") != "0")):
         # the copy engines ship each KV head's dK/dV partials as soon as the

@@ -652,9 +652,17 @@ __global__ void __maxnreg__(128)
     if (kb < 0) goto done;  // padding slot of the last cluster
     {
     const int64_t row = (int64_t)krow0 + r;
-    float* dst = (c == 0 ? p.dv : p.dk) +
-                 (p.dkv_head_major ? ((int64_t)hkv * p.k_rows * 128 + row) * 128
-                                   : (row * p.Hkv + hkv) * 128);
+    float* dst;
+    if (p.dkv_peers != nullptr) {  // fused reduce-scatter: the owner's workspace slot
+      const int owner = krow0 / p.dkv_rows_per_owner;
+      const int64_t lr = row - (int64_t)owner * p.dkv_rows_per_owner;
+      dst = p.dkv_peers[owner] +
+            (((int64_t)(c == 0 ? 1 : 0) * p.Hkv + hkv) * p.dkv_rows_per_owner + lr) * 128;
+    } else {
+      dst = (c == 0 ? p.dv : p.dk) +
+            (p.dkv_head_major ? ((int64_t)hkv * p.k_rows * 128 + row) * 128
+                              : (row * p.Hkv + hkv) * 128);
+    }
     const float mul = c == 0 ? 1.f : p.scale;
     if (nsteps > 0) {
 #if BAM_BWD_KVT
@@ -663,6 +671,40 @@ __global__ void __maxnreg__(128)
       mbar_wait_sleep(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
 #endif
       tc_fence_after();
+      if (p.dkv_peers != nullptr) {
+        // fused reduce-scatter: rows staged in the (now idle) Q/dO stages, 272-B
+        // pitch (conflict-free 16-B stores), then one 256-B bulk copy per half
+        // row; the CTA waits only for the shared-memory reads, not for the
+        // NVLink writes to land
+        static_assert(kStages * sizeof(Stage) >= 2 * 128 * 272, "staging space");
+        const uint32_t s_row = smem_u32(reinterpret_cast<uint8_t*>(&sm.st[0])) +
+                               (uint32_t)(c * 128 * 272 + r * 272);
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          if (hh) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#pragma unroll
+          for (int q2 = 0; q2 < 2; ++q2) {
+            uint32_t a[32];
+            BAM_TMEM_LD32(tmem + lane_base + (c == 0 ? kColDV : kColDK) + (hh * 2 + q2) * 32, a);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(s_row + q2 * 128 + i * 16),
+                           "f"(__uint_as_float(a[4 * i]) * mul),
+                           "f"(__uint_as_float(a[4 * i + 1]) * mul),
+                           "f"(__uint_as_float(a[4 * i + 2]) * mul),
+                           "f"(__uint_as_float(a[4 * i + 3]) * mul)
+                           : "memory");
+          }
+          fence_async_smem();
+          asm volatile(
+              "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;\n\t"
+              "cp.async.bulk.commit_group;" ::"l"(dst + hh * 64),
+              "r"(s_row)
+              : "memory");
+        }
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      } else
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
         uint32_t a[32];
@@ -886,6 +928,11 @@ static int check_bwd(const BamAttnBwdParams* pp) {
                 "bam_attn_bwd: head group [%d, %d) of Hq=%d over Hkv=%d", p.h_begin,
                 p.h_begin + nh, p.Hq, p.Hkv);
   BAM_CHECK_ARG(p.nb <= 65535, "bam_attn_bwd: nb=%d > 65535", p.nb);
+  BAM_CHECK_ARG(p.dkv_peers == nullptr ||
+                    (p.dkv_rows_per_owner >= 128 && p.dkv_rows_per_owner % 128 == 0 &&
+                     (int64_t)p.k_rows * 128 % p.dkv_rows_per_owner == 0),
+                "bam_attn_bwd: dkv_rows_per_owner=%d must be a multiple of 128 dividing %d",
+                p.dkv_rows_per_owner, p.k_rows * 128);
   return kOk;
 }
 

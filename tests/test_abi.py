@@ -34,7 +34,7 @@ def test_struct_sizes_match_header():
     assert ctypes.sizeof(_lib.BamBlockSummary) == 40
     # pointers + 5 int32 + float + 2 int32 (head group), 8-byte aligned
     assert ctypes.sizeof(_lib.BamAttnFwdParams) == 11 * 8 + 8 * 4 + 3 * 8 + 2 * 4 + 8 + 4 * 4
-    assert ctypes.sizeof(_lib.BamAttnBwdParams) == 17 * 8 + 8 * 4 + 8 + 2 * 4 + 8 + 2 * 4
+    assert ctypes.sizeof(_lib.BamAttnBwdParams) == 17 * 8 + 8 * 4 + 8 + 2 * 4 + 8 + 2 * 4 + 8 + 2 * 4
 
 
 def test_ilp_host_entry_point():
