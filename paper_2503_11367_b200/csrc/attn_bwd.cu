@@ -64,6 +64,11 @@ constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
 // staging double-buffered (BAM_DQ_STAGE2, so the single-buffered chain never
 // waits on a bulk reduce) the full kernel runs 1020-1038 vs 975-985 TFLOP/s.
 // 1 (default).  0 = double-buffered S / dP, both SS, one 32-KB dQ stage.
+// Backward epilogue through shared memory + bulk copies for local dK/dV too
+// (always for the fused reduce-scatter's peer stores)
+#ifndef BAM_EPI_BULK_LOCAL
+#define BAM_EPI_BULK_LOCAL 0
+#endif
 #ifndef BAM_BWD_KVT
 #define BAM_BWD_KVT 1
 #endif
@@ -671,7 +676,7 @@ __global__ void __maxnreg__(128)
       mbar_wait_sleep(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
 #endif
       tc_fence_after();
-      if (p.dkv_peers != nullptr) {
+      if (BAM_EPI_BULK_LOCAL || p.dkv_peers != nullptr) {
         // fused reduce-scatter: rows staged in the (now idle) Q/dO stages, 272-B
         // pitch (conflict-free 16-B stores), then one 256-B bulk copy per half
         // row; the CTA waits only for the shared-memory reads, not for the
