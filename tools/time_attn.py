@@ -16,6 +16,8 @@ from paper_2503_11367_b200.workloads import CONFIGS, SWEEP_128K  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="4")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--heads", type=int, default=0, help="override Hq")
+ap.add_argument("--kv-heads", type=int, default=0, help="override Hkv")
 args = ap.parse_args()
 out = {}
 for name in args.config.split(","):
@@ -24,6 +26,7 @@ for name in args.config.split(","):
         segs, Hq, Hkv = cfg["segments"], cfg["Hq"], cfg["Hkv"]
     else:
         segs, Hq, Hkv = SWEEP_128K[name], 32, 8
+    Hq, Hkv = args.heads or Hq, args.kv_heads or Hkv
     mask = M.build_bitfield(segs)
     desc = mask.device_descriptors()
     plan = A.build_plan(desc)
