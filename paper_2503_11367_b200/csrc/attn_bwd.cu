@@ -831,24 +831,40 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
                                  const __nv_bfloat16* __restrict__ dout,
                                  const float* __restrict__ lse, int64_t rows, int H,
                                  float* __restrict__ ld) {
+  // one warp per 4 (row, head) items: 8 independent 8-B loads in flight per lane
   const int64_t nw = rows * H;
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const uint2 a = reinterpret_cast<const uint2*>(o + w * 128)[lane_id()];
-    const uint2 b = reinterpret_cast<const uint2*>(dout + w * 128)[lane_id()];
-    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
-    float acc = 0.f;
+  const int lane = lane_id();
+  for (int64_t w0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 4; w0 < nw;
+       w0 += (((int64_t)gridDim.x * blockDim.x) >> 5) * 4) {
+    uint2 a[4], b[4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const float2 x = __bfloat1622float2(a2[i]), y = __bfloat1622float2(b2[i]);
-      acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+    for (int u = 0; u < 4; ++u) {
+      const int64_t w = w0 + u < nw ? w0 + u : nw - 1;
+      a[u] = __ldcs(reinterpret_cast<const uint2*>(o + w * 128) + lane);
+      b[u] = __ldcs(reinterpret_cast<const uint2*>(dout + w * 128) + lane);
     }
-    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-    if (lane_id() == 0) {
-      const int64_t row = w / H, h = w % H;
+    float acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b[u]);
+      float t = 0.f;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float2 x = __bfloat1622float2(a2[i]), y = __bfloat1622float2(b2[i]);
+        t = fmaf(x.x, y.x, fmaf(x.y, y.y, t));
+      }
+      acc[u] = t;
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], s);
+    if (lane < 4 && w0 + lane < nw) {
+      const float mine = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+      const int64_t w = w0 + lane, row = w / H, h = w % H;
       ld[h * 2 * rows + row] = lse[h * rows + row] * 1.4426950408889634f;
-      ld[h * 2 * rows + rows + row] = acc;
+      ld[h * 2 * rows + rows + row] = mine;
     }
   }
 }
