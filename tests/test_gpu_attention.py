@@ -106,6 +106,21 @@ def test_multimodal_partial_tiles():
     run_case(desc, 2, 2)
 
 
+def test_prefix_lm_small_gqa():
+    # config 5's prefix-LM pattern at 1K: bidirectional prefix, causal text
+    desc, _ = mask_ref.build_bitfield([("prefix", 256), ("text", 768)])
+    run_case(desc, 8, 2)
+
+
+def test_emu_interleave_small_gqa():
+    # config 4's pattern at 1K: distinct image names (bidirectional within one
+    # image only), images not block-aligned, GQA 4 query heads per KV head
+    desc, _ = mask_ref.build_bitfield([("text", 128), ("img0", 256), ("text", 64),
+                                       ("img1", 192), ("text", 128), ("img2", 128),
+                                       ("text", 128)])
+    run_case(desc, 8, 2, seed=99)
+
+
 def test_raw_descriptors():
     rng = np.random.default_rng(5)
     T = 768
