@@ -94,8 +94,7 @@ def _worker(rank, world, port, policy, result_dir):
         dist.destroy_process_group()
 
 
-def _run(policy, tmp_path):
-    world = 2
+def _run(policy, tmp_path, world=2):
     mp.spawn(_worker, args=(world, _free_port(), policy, str(tmp_path)), nprocs=world, join=True)
     for r in range(world):
         assert os.path.exists(os.path.join(tmp_path, f"ok{r}"))
@@ -107,6 +106,11 @@ def test_cp_exchange_lpt(tmp_path):
 
 def test_cp_exchange_zigzag(tmp_path):
     _run("zigzag", tmp_path)
+
+
+def test_cp_exchange_lpt_world4(tmp_path):
+    # uneven per-rank block counts and padded shards across four ranks
+    _run("lpt", tmp_path, world=4)
 
 
 def test_cp_layout_unequal_counts():
