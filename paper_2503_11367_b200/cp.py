@@ -188,6 +188,8 @@ class SymmExchange:
     def _fan_out(self, copies):
         """Run copies[r]() on peer stream r, joined back into the current stream."""
         cur = torch.cuda.current_stream()
+        while len(self.streams) < len(copies):
+            self.streams.append(torch.cuda.Stream(device=cur.device))
         start = torch.cuda.Event()
         start.record(cur)
         done = []
@@ -236,16 +238,20 @@ class SymmExchange:
         self.epoch += 1
         epoch = self.epoch
 
-        def pull(r):
+        # BAM_CP_PULL_SPLIT > 1 deals each peer's heads round-robin over that many copy
+        # streams; measured neutral at N=2/4 (profiles/r01/multi_gpu/exchange_bw), so 1
+        split = max(1, min(nkv, int(os.environ.get("BAM_CP_PULL_SPLIT", "1"))))
+
+        def pull(r, j):
             def fn():
                 src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, self.kv_off[gi])
-                for h in range(nkv):
+                for h in range(j, nkv, split):
                     k_all[h, r * rows:(r + 1) * rows].copy_(src[0, h])
                     v_all[h, r * rows:(r + 1) * rows].copy_(src[1, h])
                     _lib.call("bam_stream_write_i32", self.flags[r * nkv + h:].data_ptr(), epoch)
             return fn
         peers = [(self.rank + step) % self.world for step in range(1, self.world)]
-        self._fan_out([pull(r) for r in peers])
+        self._fan_out([pull(r, j) for j in range(split) for r in peers])
         for t in (k_all, v_all):
             for st in self.streams:
                 t.record_stream(st)
