@@ -21,6 +21,7 @@ materialised lazily on first access.
 from __future__ import annotations
 
 import json
+from dataclasses import dataclass
 from typing import Iterable, Sequence
 
 import torch
@@ -61,66 +62,86 @@ def _to_int64(d: int) -> int:
     return d - (1 << 64) if d >= 1 << 63 else d
 
 
+class _Lazy:
+    """Data descriptor behind a frozen-dataclass field whose value may be
+    derived on first access from device tensors (``build(obj)``).  The
+    dataclass machinery sees a required field (``__get__`` on the class
+    raises AttributeError, so there is no default); ``__init__`` and
+    ``dataclasses.replace`` store through ``__set__``; assignment on an
+    instance still raises ``FrozenInstanceError``."""
+
+    def __init__(self, build):
+        self.build = build
+
+    def __set_name__(self, owner, name):
+        self.slot = "_v_" + name
+
+    def __get__(self, obj, owner=None):
+        if obj is None:
+            raise AttributeError(self.slot)
+        d = obj.__dict__
+        if self.slot not in d:
+            d[self.slot] = self.build(obj)
+        return d[self.slot]
+
+    def __set__(self, obj, value):
+        obj.__dict__[self.slot] = value
+
+
+def _descriptors_from_device(mask) -> tuple:
+    vals = mask.__dict__["_dev"].cpu().tolist()
+    return tuple(v + (1 << 64) if v < 0 else v for v in vals)
+
+
+@dataclass(frozen=True)
 class BitfieldMask:
-    """Per-token descriptors for one packed sequence (mask.py:43-68).
+    """Per-token descriptors for one packed sequence (mask.py:43-68): the
+    reference's frozen dataclass, same fields (``dataclasses.fields``,
+    ``asdict``, ``replace`` and equality behave identically).
 
     ``descriptors`` (tuple of ints) and ``modalities`` (registration order;
-    modality i uses bit i+1) behave as in the reference frozen dataclass.
-    ``device_descriptors()`` is the int64 CUDA tensor the kernels use.
+    modality i uses bit i+1).  Masks built on the GPU keep their int64
+    descriptors on the device (``device_descriptors()``, not a dataclass
+    field); the tuple is materialised on first access.
     """
 
-    __slots__ = ("_desc", "_dev", "modalities", "_out_of_range")
+    descriptors: tuple = _Lazy(_descriptors_from_device)
+    modalities: tuple
 
-    def __init__(self, descriptors=(), modalities: Sequence[str] = ()):
-        object.__setattr__(self, "modalities", tuple(modalities))
-        if isinstance(descriptors, torch.Tensor):
-            object.__setattr__(self, "_desc", None)
-            object.__setattr__(self, "_dev", descriptors.to(torch.int64))
-            object.__setattr__(self, "_out_of_range", None)
-        else:
-            desc = tuple(int(d) for d in descriptors)
-            object.__setattr__(self, "_desc", desc)
-            object.__setattr__(self, "_dev", None)
-            bad = None
-            for t, d in enumerate(desc):
-                if not 0 <= d < 1 << 64:
-                    bad = t
-                    break
-            object.__setattr__(self, "_out_of_range", bad)
-
-    def __setattr__(self, name, value):
-        raise AttributeError("BitfieldMask is immutable")
-
-    @property
-    def descriptors(self) -> tuple:
-        if self._desc is None:
-            vals = self._dev.cpu().tolist()
-            object.__setattr__(self, "_desc", tuple(v + (1 << 64) if v < 0 else v for v in vals))
-        return self._desc
+    @classmethod
+    def _from_device(cls, desc: torch.Tensor, modalities: Sequence[str]) -> "BitfieldMask":
+        obj = object.__new__(cls)
+        obj.__dict__["_dev"] = desc.to(torch.int64)
+        object.__setattr__(obj, "modalities", tuple(modalities))
+        return obj
 
     def __len__(self) -> int:
-        return self._dev.shape[0] if self._desc is None else len(self._desc)
+        d = self.__dict__
+        if "_v_descriptors" not in d and d.get("_dev") is not None:
+            return int(d["_dev"].shape[0])
+        return len(self.descriptors)
 
-    def __eq__(self, other) -> bool:
-        if not isinstance(other, BitfieldMask):
-            return NotImplemented
-        return self.modalities == other.modalities and self.descriptors == other.descriptors
-
-    def __hash__(self) -> int:
-        return hash((self.descriptors, self.modalities))
-
-    def __repr__(self) -> str:
-        return f"BitfieldMask(len={len(self)}, modalities={self.modalities!r})"
+    def _first_out_of_range(self):
+        if "_v_descriptors" not in self.__dict__:
+            return None            # device-built: int64 by construction
+        for t, d in enumerate(self.descriptors):
+            if not 0 <= d < 1 << 64:
+                return t
+        return None
 
     def device_descriptors(self) -> torch.Tensor:
-        """int64 [T] descriptors on the current CUDA device (cached)."""
-        if self._dev is None:
+        """int64 [T] descriptors on the current CUDA device (cached; not a
+        dataclass field).  Out-of-range values (rejected by ``validate``)
+        are replaced by 1 here."""
+        dev_t = self.__dict__.get("_dev")
+        if dev_t is None:
             dev = _device()
-            vals = [_to_int64(d) if 0 <= d < 1 << 64 else 1 for d in self._desc]
-            object.__setattr__(self, "_dev", torch.tensor(vals, dtype=torch.int64, device=dev))
-        elif self._dev.device.type != "cuda":
-            object.__setattr__(self, "_dev", self._dev.to(_device()))
-        return self._dev
+            vals = [_to_int64(d) if 0 <= d < 1 << 64 else 1 for d in self.descriptors]
+            dev_t = torch.tensor(vals, dtype=torch.int64, device=dev)
+        elif dev_t.device.type != "cuda":
+            dev_t = dev_t.to(_device())
+        self.__dict__["_dev"] = dev_t
+        return dev_t
 
     def validate(self) -> None:
         """mask.py:53-68 -- raises MaskError for the first failing token."""
@@ -134,7 +155,7 @@ class BitfieldMask:
         err = torch.empty(1, dtype=torch.int64, device=desc.device)
         _lib.call("bam_mask_validate", desc.data_ptr(), T, err.data_ptr())
         code = int(err.item()) & 0xFFFFFFFFFFFFFFFF
-        first_range = self._out_of_range
+        first_range = self._first_out_of_range()
         if code == 0xFFFFFFFFFFFFFFFF and first_range is None:
             return
         tok, kind = (code >> 2, code & 3) if code != 0xFFFFFFFFFFFFFFFF else (None, 0)
@@ -171,7 +192,7 @@ def build_bitfield(segments: Sequence[tuple[str, int]]) -> BitfieldMask:
     se = torch.tensor(seg_end, dtype=torch.int64, device=dev)
     desc = torch.empty(total, dtype=torch.int64, device=dev)
     _lib.call("bam_mask_expand", sd.data_ptr(), se.data_ptr(), len(seg_desc), total, desc.data_ptr())
-    mask = BitfieldMask(desc, modalities)
+    mask = BitfieldMask._from_device(desc, modalities)
     mask.validate()
     return mask
 
@@ -185,48 +206,64 @@ def materialize(mask: BitfieldMask, q: int, k: int) -> bool:
     return dk == dq
 
 
-class BlockWorkload:
-    """Blockwise classification and per-query-block work (mask.py:115-125).
+def _classes_from_device(work) -> tuple:
+    rows = work.__dict__["class_codes"].cpu().tolist()
+    return tuple(tuple(CLASS_NAMES[c] for c in row) for row in rows)
 
-    ``classes`` ([query block][key block] strings) and ``workloads`` are the
-    reference views; ``class_codes`` (uint8 [nb, nb], 0 skip / 1 full /
-    2 partial) and ``workload_tensor`` (int32 [nb]) stay on the device.
+
+def _workloads_from_device(work) -> tuple:
+    return tuple(work.__dict__["workload_tensor"].cpu().tolist())
+
+
+@dataclass(frozen=True)
+class BlockWorkload:
+    """Blockwise classification and per-query-block work (mask.py:115-125):
+    the reference's frozen dataclass with the same fields.
+
+    ``classes`` ([query block][key block] strings) and ``workloads`` are
+    materialised on first access from the device results, which stay
+    available as ``class_codes`` (uint8 [nb, nb], 0 skip / 1 full /
+    2 partial) and ``workload_tensor`` (int32 [nb]) -- attributes, not
+    dataclass fields.
     """
 
-    __slots__ = ("block_size", "class_codes", "workload_tensor", "_classes", "_workloads")
+    block_size: int
+    classes: tuple = _Lazy(_classes_from_device)
+    workloads: tuple = _Lazy(_workloads_from_device)
 
-    def __init__(self, block_size: int, class_codes: torch.Tensor, workload_tensor: torch.Tensor):
-        self.block_size = block_size
-        self.class_codes = class_codes
-        self.workload_tensor = workload_tensor
-        self._classes = None
-        self._workloads = None
-
-    @property
-    def classes(self) -> tuple:
-        if self._classes is None:
-            rows = self.class_codes.cpu().tolist()
-            self._classes = tuple(tuple(CLASS_NAMES[c] for c in row) for row in rows)
-        return self._classes
-
-    @property
-    def workloads(self) -> tuple:
-        if self._workloads is None:
-            self._workloads = tuple(self.workload_tensor.cpu().tolist())
-        return self._workloads
+    @classmethod
+    def _from_device(cls, block_size: int, class_codes: torch.Tensor,
+                     workload_tensor: torch.Tensor) -> "BlockWorkload":
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "block_size", block_size)
+        obj.__dict__["class_codes"] = class_codes
+        obj.__dict__["workload_tensor"] = workload_tensor
+        return obj
 
     @property
     def num_blocks(self) -> int:
-        return int(self.workload_tensor.shape[0])
+        wt = self.__dict__.get("workload_tensor")
+        if "_v_workloads" not in self.__dict__ and wt is not None:
+            return int(wt.shape[0])
+        return len(self.workloads)
 
-    def __eq__(self, other) -> bool:
-        if not isinstance(other, BlockWorkload):
-            return NotImplemented
-        return (self.block_size == other.block_size and self.workloads == other.workloads
-                and torch.equal(self.class_codes.cpu(), other.class_codes.cpu()))
+    @property
+    def class_codes(self) -> torch.Tensor:
+        t = self.__dict__.get("class_codes")
+        if t is None:
+            codes = [[CLASS_NAMES.index(c) for c in row] for row in self.classes]
+            t = torch.tensor(codes, dtype=torch.uint8, device=_device()).reshape(
+                len(codes), len(codes[0]) if codes else 0)
+            self.__dict__["class_codes"] = t
+        return t
 
-    def __repr__(self) -> str:
-        return f"BlockWorkload(block_size={self.block_size}, num_blocks={self.num_blocks})"
+    @property
+    def workload_tensor(self) -> torch.Tensor:
+        t = self.__dict__.get("workload_tensor")
+        if t is None:
+            t = torch.tensor(list(self.workloads), dtype=torch.int32, device=_device())
+            self.__dict__["workload_tensor"] = t
+        return t
 
 
 def block_summaries(desc: torch.Tensor, block_size: int) -> torch.Tensor:
@@ -276,10 +313,11 @@ def block_workloads(mask: BitfieldMask, block_size: int = DEFAULT_BLOCK_SIZE) ->
     mask.validate()
     if len(mask) == 0:
         dev = _device()
-        return BlockWorkload(block_size, torch.empty(0, 0, dtype=torch.uint8, device=dev),
-                             torch.empty(0, dtype=torch.int32, device=dev))
+        return BlockWorkload._from_device(block_size,
+                                          torch.empty(0, 0, dtype=torch.uint8, device=dev),
+                                          torch.empty(0, dtype=torch.int32, device=dev))
     classes, W = classify_device(mask.device_descriptors(), block_size)
-    return BlockWorkload(block_size, classes, W)
+    return BlockWorkload._from_device(block_size, classes, W)
 
 
 # --- documents (mask.py:193-252) -------------------------------------------

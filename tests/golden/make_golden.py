@@ -193,6 +193,17 @@ def main():
                     f"import sys; sys.path.insert(0, {REF_SRC!r}); from mmplan.cli import main; "
                     f"sys.exit(main(['cp-distribute', '--mask', {fixture!r}, '-o', {out!r}]))"],
                    check=True)
+    # the reference's own pinned invocation (ref tests/test_cli.py:46-53), checked here
+    # against the reference's committed golden (ref tests/golden/report_two_encoders.json)
+    out_ilp = os.path.join(HERE, "report_two_encoders_ilp.json")
+    subprocess.run([sys.executable, "-c",
+                    f"import sys; sys.path.insert(0, {REF_SRC!r}); from mmplan.cli import main; "
+                    f"sys.exit(main(['cp-distribute', '--mask', {fixture!r}, '-g', '4', '-c', '2', "
+                    f"'-s', '2', '--ilp', '-o', {out_ilp!r}]))"],
+                   check=True)
+    with open(out_ilp, "rb") as a, open("/root/reference/pkg/tests/golden/report_two_encoders.json",
+                                        "rb") as b:
+        assert a.read() == b.read(), "reference CLI no longer reproduces its own golden"
     if "--skip-configs" not in sys.argv:
         write("config1_workloads.json",
               config_workloads([("text", 128), ("image", 1024), ("text", 2944)], "config1"))

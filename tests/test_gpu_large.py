@@ -34,13 +34,26 @@ def check(name, got, ref):
 
 @pytest.mark.parametrize("cfg_id", [2, 3, 4])
 def test_full_size_config(cfg_id):
-    from paper_2503_11367_b200 import attention as A, mask as M
     from paper_2503_11367_b200.workloads import CONFIGS
 
     cfg = CONFIGS[cfg_id]
-    Hq, Hkv = cfg["Hq"], cfg["Hkv"]
+    _full_size_parity(cfg["segments"], cfg["Hq"], cfg["Hkv"])
+
+
+@pytest.mark.parametrize("name", ["causal", "prefix_lm", "multimodal"])
+def test_full_size_sweep_128k(name):
+    """BASELINE.json config 5: the 128K mask sweep at GQA 32q/8kv (multi_image
+    is config 4 above).  The causal mask exercises 1024-entry tile lists."""
+    from paper_2503_11367_b200.workloads import SWEEP_128K
+
+    _full_size_parity(SWEEP_128K[name], 32, 8)
+
+
+def _full_size_parity(segments, Hq, Hkv):
+    from paper_2503_11367_b200 import attention as A, mask as M
+
     grp = Hq // Hkv
-    mask = M.build_bitfield(cfg["segments"])
+    mask = M.build_bitfield(segments)
     desc_d = mask.device_descriptors()
     T = desc_d.shape[0]
     nb = T // 128

@@ -118,6 +118,18 @@ def test_oracle_balance_vs_reference_golden():
         assert balance_ref.balance_report(w, G, it["compute_units"], it["subblock_size"]) == case["report"]
 
 
+def test_oracle_reference_cli_golden_ilp():
+    # ref tests/test_cli.py:46-53: cp-distribute -g 4 -c 2 -s 2 --ilp on the reference fixture
+    doc = load_golden("report_two_encoders_ilp.json")
+    fx = load_golden("mask_two_encoders_fixture.json")
+    d, _ = mask_ref.build_bitfield([(s["modality"], s["count"]) for s in fx["segments"]])
+    _, W = mask_ref.block_workloads_np(np.asarray(d, np.int64), 128)
+    assert list(W) == doc["workloads"] == [1, 2, 2, 4, 5, 2, 2, 8]
+    assert (doc["gpus"], doc["compute_units"], doc["subblock_size"]) == (4, 2, 2)
+    assert balance_ref.balance_report(list(W), 4, 2, 2) == doc["policies"]
+    assert balance_ref.makespan_exhaustive(list(W), 4) == doc["ilp_optimal"]["makespan"] == 8
+
+
 def test_attention_oracle_vs_dense_autograd():
     d, _ = mask_ref.build_bitfield([("text", 40), ("img", 50), ("text", 38)])
     T = len(d)
