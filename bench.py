@@ -82,9 +82,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-blocks", type=int, default=2)
-    ap.add_argument("--transport", default="ce", choices=["nccl", "ce"],
-                    help="CP exchange: NCCL collectives or copy-engine pulls/pushes over "
-                         "symmetric memory (N > 1)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "ce"],
+                    help="CP exchange (N > 1): copy-engine pulls/pushes over symmetric memory "
+                         "('ce'), NCCL collectives, or 'auto' = ce when every rank can map its "
+                         "peers, else NCCL (agreed collectively)")
     ap.add_argument("--groups", type=int, default=1,
                     help="KV-head groups pipelining the CP collectives with compute (N > 1); "
                          "1 measured best at N=2/4 (profiles/r01/head_group_ablation.md)")
@@ -254,30 +255,20 @@ def main():
     flop_local_bwd = 10.0 * D * Hq * n_allowed / world
 
     n_groups = args.groups if world > 1 else 1
-    if world > 1 and args.transport == "ce":
-        try:   # symmetric-memory rendezvous; NCCL collectives if the box cannot map peers
-            plan.exchange(CP._head_groups(Hkv, n_groups), D, dev)
-        except Exception as exc:  # noqa: BLE001
-            print(f"bench: copy-engine transport unavailable ({exc}); using NCCL", file=sys.stderr)
-            args.transport = "nccl"
+    # transport agreed collectively ("auto": copy engines when peer memory maps on every
+    # rank, else NCCL); at N=1 there is no exchange
+    transport = CP.resolve_transport(args.transport, plan, Hkv, D, dev)
 
     def step(ev):
-        """ev: [fwd start, fwd end, bwd end, (main start, main end) per head group...]"""
-        if world > 1:
-            ev[0].record()
-            o, lse, gathered = CP.cp_forward(q_loc, k_loc, v_loc, plan, groups=n_groups,
-                                             transport=args.transport)
-            ev[1].record()
-            timers = [(ev[3 + 2 * i], ev[4 + 2 * i]) for i in range(len(gathered))]
-            dq, dk, dv = CP.cp_backward(q_loc, gathered, o, lse, do_loc, plan, timers=timers,
-                                        transport=args.transport)
-            ev[2].record()
-            return dq, dk, dv
+        """ev: [step start, fwd end, bwd end, fwd kernels start/end, bwd main start/end...]:
+        the kernel-only pairs exclude the exchange barriers and waits"""
         ev[0].record()
-        o, lse = A.attn_forward(q_loc, k_loc, v_loc, plan.attn)
+        o, lse, gathered = CP.cp_forward(q_loc, k_loc, v_loc, plan, groups=n_groups,
+                                         transport=transport, timer=(ev[3], ev[4]))
         ev[1].record()
-        dq, dk, dv = A.attn_backward(q_loc, k_loc, v_loc, o, lse, do_loc, plan.attn,
-                                     timer=(ev[3], ev[4]))
+        timers = [(ev[5 + 2 * i], ev[6 + 2 * i]) for i in range(len(gathered))]
+        dq, dk, dv = CP.cp_backward(q_loc, gathered, o, lse, do_loc, plan, timers=timers,
+                                    transport=transport)
         ev[2].record()
         return dq, dk, dv
 
@@ -287,21 +278,10 @@ def main():
         torch.cuda.synchronize()
 
     mk = lambda: [torch.cuda.Event(enable_timing=True)  # noqa: E731
-                  for _ in range(3 + 2 * n_groups)]
-    try:
-        for _ in range(args.warmup):
-            step(mk())
-        barrier()
-    except Exception as exc:  # noqa: BLE001
-        if world == 1 or args.transport != "ce":
-            raise
-        # the copy-engine transport failed on this box: NCCL collectives instead
-        print(f"bench: copy-engine transport failed in warm-up ({exc}); using NCCL",
-              file=sys.stderr)
-        args.transport = "nccl"
-        for _ in range(args.warmup):
-            step(mk())
-        barrier()
+                  for _ in range(5 + 2 * n_groups)]
+    for _ in range(args.warmup):
+        step(mk())
+    barrier()
     evs = [mk() for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.launch_count
@@ -315,21 +295,29 @@ def main():
     launches = _lib.launch_count - launches0
     elapsed = start.elapsed_time(end)
     fwd_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    bwd_main_ms = sum(e[3 + 2 * i].elapsed_time(e[4 + 2 * i])
-                      for e in evs for i in range(n_groups)) / args.steps
     bwd_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    compute_ms = fwd_ms + bwd_ms
-    t = torch.tensor([elapsed, compute_ms], dtype=torch.float64, device=dev)
+    fwd_kernel_ms = sum(e[3].elapsed_time(e[4]) for e in evs) / args.steps
+    bwd_main_ms = sum(e[5 + 2 * i].elapsed_time(e[6 + 2 * i])
+                      for e in evs for i in range(n_groups)) / args.steps
+    # per-rank kernel-only time: the forward kernels + the backward main kernel(s); the
+    # step windows (fwd_ms + bwd_ms) end at exchange barriers, i.e. with the slowest rank
+    kernel_ms = fwd_kernel_ms + bwd_main_ms
+    t = torch.tensor([elapsed, kernel_ms, fwd_ms + bwd_ms], dtype=torch.float64, device=dev)
+    per_rank_kernel_ms = [kernel_ms]
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t.clone()
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        allk = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(world)]
+        dist.all_gather(allk, t[1:2].clone())
+        per_rank_kernel_ms = [x.item() for x in allk]
         elapsed_max = tmax[0].item()
         imb_meas = tmax[1].item() / (tsum[1].item() / world)
+        imb_window = tmax[2].item() / (tsum[2].item() / world)
     else:
         elapsed_max = elapsed
-        imb_meas = 1.0
+        imb_meas = imb_window = 1.0
     ms_step = elapsed_max / args.steps
     value = flop_step / (ms_step * 1e-3) / 1e12
 
@@ -378,7 +366,7 @@ def main():
             dod = dev_in[b][3]
             if world > 1:
                 o = CP.cp_bitfield_attention(qd, kd, vd, plan, groups=n_groups,
-                                             transport=args.transport)
+                                             transport=transport)
             else:
                 o = A.bitfield_attention(qd, kd, vd, plan.attn)
             ev_fwd[b].record(cur)
@@ -426,7 +414,9 @@ def main():
     peak = peaks.get("bf16_tflops_sustained", peak_burst)
     peak_kind = "bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "bf16_tflops"
     bwd_achieved = flop_local_bwd / (bwd_main_ms * 1e-3) / 1e12
-    fwd_achieved = flop_local_fwd / (fwd_ms * 1e-3) / 1e12
+    fwd_achieved = flop_local_fwd / (fwd_kernel_ms * 1e-3) / 1e12
+    fwd_kernel = ("bam attn_fwd_split_kernel (GQA head pairs)" if (Hq // Hkv) % 2 == 0 else
+                  "bam attn_fwd_split_kernel (MHA query-block pairs) + attn_fwd_kernel (rest)")
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -447,15 +437,21 @@ def main():
             "config": {"workload": cfg["name"], "tokens": T, "Hq": Hq, "Hkv": Hkv, "head_dim": D,
                        "cp": world, "policy": args.policy, "n_allowed": n_allowed,
                        "kv_head_groups": n_groups,
-                       "transport": args.transport if world > 1 else None,
+                       "transport": transport if world > 1 else None,
                        "flop_per_step": flop_step,
                        "l2": "inputs larger than L2 (Q alone %.2f GiB per rank)" %
                              (q_loc.numel() * 2 / 2**30)},
             "tflops_per_gpu": value / world,
             "frac_of_peak": value / world / peak,
             "frac_of_burst_peak": value / world / peak_burst,
-            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "bwd_main_ms": bwd_main_ms,
+            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "fwd_kernel_ms": fwd_kernel_ms,
+            "bwd_main_ms": bwd_main_ms,
             "imbalance_predicted": imb_pred, "imbalance_measured": imb_meas,
+            "imbalance_measured_basis": "max/mean over ranks of per-rank kernel-only time "
+                                        "(forward kernels + backward main kernel, CUDA events "
+                                        "around the launches; no exchange barrier inside)",
+            "per_rank_kernel_ms": per_rank_kernel_ms,
+            "imbalance_step_window": imb_window,
             "roofline": {"bound": "tensor", "kernel": "bam attn_bwd_kernel (tcgen05)",
                          "achieved": bwd_achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": bwd_achieved / peak, "traffic": traffic,
@@ -463,7 +459,7 @@ def main():
                          "peak_source": peak_src + " " + peak_kind +
                          " (kernel timed inside a long step)",
                          "peak_burst": peak_burst, "frac_of_burst": bwd_achieved / peak_burst,
-                         "fwd": {"kernel": "bam attn_fwd_split_kernel (GQA head pairs)", "achieved": fwd_achieved,
+                         "fwd": {"kernel": fwd_kernel, "achieved": fwd_achieved,
                                  "frac": fwd_achieved / peak,
                                  "frac_of_burst": fwd_achieved / peak_burst}},
             "cpu_baseline": cpu_baseline,

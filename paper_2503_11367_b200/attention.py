@@ -238,8 +238,11 @@ def build_split_schedule(plan: AttentionPlan, subblock: int) -> SplitSchedule:
 
 def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
                  h_begin: int = 0, nh: int = 0, out=None, schedule: SplitSchedule | None = None,
-                 kv_ready=None, kv_head_major: bool = False):
+                 kv_ready=None, kv_head_major: bool = False, timer=None):
     """Returns (o bf16 [nq*128, Hq, 128], lse fp32 [Hq, nq*128]).
+
+    ``timer=(start, end)``: CUDA events recorded right before the first and
+    after the last kernel launch (kernel-only time).
 
     ``kv_head_major``: k/v are [Hkv, k_rows*128, 128] instead of token-major
     (then ``kv_ready`` flags are per (rank, KV head): ``flags[owner*Hkv + hkv]``).
@@ -290,51 +293,45 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         if schedule is not None:
             raise ValueError("kv_ready needs whole rows")
         flags, epoch, rank, rows_per_rank = kv_ready
+        if rows_per_rank < 1 or plan.k_rows // rows_per_rank > 64 or not 0 <= rank < 64:
+            raise ValueError("kv_ready: rows_per_rank >= 1, at most 64 ranks")
         p.kv_ready, p.kv_epoch, p.kv_rank, p.kv_rows_per_rank = (flags.data_ptr(), int(epoch),
                                                                  int(rank), int(rows_per_rank))
-        if (nh // Hkv) % 2 == 0 or plan.fwd_pair_ids is None:
-            _lib.call("bam_attn_fwd", p)
-            return o, lse
-        _lib.call("bam_attn_fwd_qpairs", p, plan.fwd_pair_ids.data_ptr(),
-                  int(plan.fwd_pair_ids.shape[0]), plan.fwd_slot_q.data_ptr(),
-                  plan.fwd_slot_off.data_ptr(), plan.fwd_slot_tiles.data_ptr())
-        n_rest = int(plan.fwd_rest_items.shape[0])
-        if n_rest:
-            p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
-            _lib.call("bam_attn_fwd", p)
-        return o, lse
-    if (schedule is None and plan.fwd_pair_ids is not None and (nh // Hkv) % 2 == 0
-            and os.environ.get("BAM_FWD_2CTA", "0") == "1"):
-        # shared query-block pairs on CTA pairs, the rest as whole-row items.  Opt-in:
-        # measured 1084-1106 vs 1137-1143 TFLOP/s for the one-CTA head-pair kernel on
-        # config 4 -- the forward is bound by MUFU / softmax latency, not by the K/V
-        # operand traffic the CTA pair halves (profiles/r01/fwd_2cta.md)
-        n_pairs = int(plan.fwd_pair_ids.shape[0])
-        _lib.call("bam_attn_fwd_2cta", p, plan.fwd_pair_ids.data_ptr(), n_pairs,
-                  plan.fwd_slot_q.data_ptr(), plan.fwd_slot_off.data_ptr(),
-                  plan.fwd_slot_tiles.data_ptr())
-        n_rest = int(plan.fwd_rest_items.shape[0])
-        if n_rest:
-            p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
-            _lib.call("bam_attn_fwd", p)
-        return o, lse
-    if (schedule is None and plan.fwd_pair_ids is not None and (nh // Hkv) % 2 == 1
-            and os.environ.get("BAM_FWD_QPAIRS", "1") != "0"):
-        # MHA: shared query-block pairs share K/V tiles in one split-row CTA; the
-        # blocks of the other pairs run as whole-row items of the one-head kernel
-        _lib.call("bam_attn_fwd_qpairs", p, plan.fwd_pair_ids.data_ptr(),
-                  int(plan.fwd_pair_ids.shape[0]), plan.fwd_slot_q.data_ptr(),
-                  plan.fwd_slot_off.data_ptr(), plan.fwd_slot_tiles.data_ptr())
-        n_rest = int(plan.fwd_rest_items.shape[0])
-        if n_rest:
-            p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
-            _lib.call("bam_attn_fwd", p)
-        return o, lse
-    _lib.call("bam_attn_fwd", p)
-    if schedule is not None and schedule.combine.shape[0]:
-        _lib.call("bam_attn_fwd_combine", p, schedule.combine.data_ptr(),
-                  int(schedule.combine.shape[0]))
+    if timer is not None:
+        timer[0].record()
+    _launch_fwd(p, plan, schedule, (nh // Hkv) % 2 == 0, kv_ready is not None)
+    if timer is not None:
+        timer[1].record()
     return o, lse
+
+
+def _launch_fwd(p, plan: AttentionPlan, schedule, pair_heads: bool, flagged: bool):
+    """Kernel choice.  GQA (an even number of query heads per KV head): the
+    split-row head-pair kernel.  MHA: shared query-block pairs in the
+    split-row kernel, the other blocks as whole-row items of the one-head
+    kernel.  Split-KV schedules: the one-head kernel + the combine."""
+    pairs = schedule is None and plan.fwd_pair_ids is not None
+    if pairs and not pair_heads and (flagged or os.environ.get("BAM_FWD_QPAIRS", "1") != "0"):
+        entry = "bam_attn_fwd_qpairs"
+    elif pairs and pair_heads and not flagged and os.environ.get("BAM_FWD_2CTA", "0") == "1":
+        # shared query-block pairs on CTA pairs (cta_group::2).  Opt-in: measured
+        # 1084-1106 vs 1137-1143 TFLOP/s for the one-CTA head-pair kernel on config 4 --
+        # the forward is bound by MUFU / softmax latency, not by the K/V operand traffic
+        # the CTA pair halves (profiles/r01/fwd_2cta.md)
+        entry = "bam_attn_fwd_2cta"
+    else:
+        _lib.call("bam_attn_fwd", p)
+        if schedule is not None and schedule.combine.shape[0]:
+            _lib.call("bam_attn_fwd_combine", p, schedule.combine.data_ptr(),
+                      int(schedule.combine.shape[0]))
+        return
+    _lib.call(entry, p, plan.fwd_pair_ids.data_ptr(), int(plan.fwd_pair_ids.shape[0]),
+              plan.fwd_slot_q.data_ptr(), plan.fwd_slot_off.data_ptr(),
+              plan.fwd_slot_tiles.data_ptr())
+    n_rest = int(plan.fwd_rest_items.shape[0])
+    if n_rest:
+        p.items, p.n_items = plan.fwd_rest_items.data_ptr(), n_rest
+        _lib.call("bam_attn_fwd", p)
 
 
 class BackwardWorkspace:

@@ -25,7 +25,6 @@ of group g overlaps the backward kernel of group g+1.
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass
 
 import torch
@@ -158,32 +157,37 @@ class SymmExchange:
     memory (torch symmetric memory, CUDA IPC).  Every rank's
     K/V shard lives in a symmetric buffer that the peers PULL with
     cudaMemcpyAsync, and the dK/dV partials are PUSHED into the owners'
-    symmetric workspaces, so the transfers run on the copy engines and take
-    no SMs from the attention kernels (NCCL's kernels do).  Per KV-head group
-    the buffers are contiguous, so one copy moves one rank's group slice."""
+    symmetric workspaces (or stored there by the backward kernel's epilogue),
+    so the transfers run on the copy engines and take no SMs from the
+    attention kernels (NCCL's kernels do).
 
-    def __init__(self, layout: CPLayout, head_groups, d: int, device, group=None):
+    The symmetric buffers are sized for a CAPACITY of ``cap_rows`` padded
+    rows per rank; every call takes the plan's own ``rows`` (its
+    ``max_blocks * 128`` <= capacity) and packs the data densely for that
+    shape, so plans of different shapes -- a new mask every batch changes
+    the LPT block counts -- reuse one exchange (``CPPlan.exchange``)."""
+
+    def __init__(self, cap_rows: int, hkv: int, d: int, world: int, rank: int, device,
+                 group=None):
         import torch.distributed._symmetric_memory as symm_mem
 
         pg = group if group is not None else dist.group.WORLD
-        self.world, self.rank = layout.world, layout.rank
-        self.rows, self.d = layout.max_blocks * BLOCK, d
-        self.kv_off, self.ws_off = [], []
-        kv_n = ws_n = 0
-        for _, nkv in head_groups:
-            per = self.rows * nkv * d
-            self.kv_off.append(kv_n)
-            self.ws_off.append(ws_n)
-            kv_n += 2 * per
-            ws_n += self.world * 2 * per
-        self.kv = symm_mem.empty((kv_n,), dtype=torch.bfloat16, device=device)
+        self.world, self.rank, self.d, self.hkv = world, rank, d, hkv
+        self.cap_rows = cap_rows
+        self.kv = symm_mem.empty((2 * cap_rows * hkv * d,), dtype=torch.bfloat16, device=device)
         self.kv_h = symm_mem.rendezvous(self.kv, pg.group_name)
-        self.ws = symm_mem.empty((ws_n,), dtype=torch.float32, device=device)
+        self.ws = symm_mem.empty((world * 2 * cap_rows * hkv * d,), dtype=torch.float32,
+                                 device=device)
         self.ws_h = symm_mem.rendezvous(self.ws, pg.group_name)
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
         self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
         self._cache = {}
+
+    def _check(self, rows: int, kv0: int, nkv: int):
+        if rows > self.cap_rows or kv0 + nkv > self.hkv:
+            raise ValueError(f"exchange capacity {self.cap_rows} rows x {self.hkv} KV heads "
+                             f"< plan {rows} rows, heads [{kv0}, {kv0 + nkv})")
 
     def _fan_out(self, copies):
         """Run copies[r]() on peer stream r, joined back into the current stream."""
@@ -204,9 +208,8 @@ class SymmExchange:
         for ev in done:
             cur.wait_event(ev)
 
-    def gather_overlapped(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor,
-                          head_major: bool = True):
-        """gather() that lets the attention start early, into HEAD-MAJOR
+    def gather_overlapped(self, rows: int, k_g: torch.Tensor, v_g: torch.Tensor):
+        """K/V all-gather that lets the attention start early, into HEAD-MAJOR
         buffers [nkv, world*rows, d]: this rank's rows go straight into the
         gathered buffers before the barrier (event ``ev_local``); the peers'
         shards are pulled one KV head at a time (one contiguous chunk per
@@ -214,14 +217,11 @@ class SymmExchange:
         ``flags[peer*nkv + h] = epoch`` (bam_stream_write_i32, no SM) that the
         forward kernel waits on per tile, so the first heads' tiles start
         after 1/nkv of the transfer.  ``ev_all``: every pull landed.
-        head_major=False: token-major buffers, one chunk and flag per peer.
         Returns (k_all, v_all, ev_local, ev_all, (flags, epoch))."""
-        nkv, rows, d = k_g.shape[1], self.rows, self.d
+        nkv, d = k_g.shape[1], self.d
+        self._check(rows, 0, nkv)
         n = k_g.shape[0]
-        per = rows * nkv * d
-        if not head_major:
-            return self._gather_overlapped_token_major(gi, k_g, v_g)
-        mine = self.kv[self.kv_off[gi]:self.kv_off[gi] + 2 * per].view(2, nkv, rows, d)
+        mine = self.kv[:2 * rows * nkv * d].view(2, nkv, rows, d)
         mine[0, :, :n].copy_(k_g.transpose(0, 1))
         mine[1, :, :n].copy_(v_g.transpose(0, 1))
         k_all = torch.empty((nkv, self.world * rows, d), dtype=k_g.dtype, device=k_g.device)
@@ -238,20 +238,15 @@ class SymmExchange:
         self.epoch += 1
         epoch = self.epoch
 
-        # BAM_CP_PULL_SPLIT > 1 deals each peer's heads round-robin over that many copy
-        # streams; measured neutral at N=2/4 (profiles/r01/multi_gpu/exchange_bw), so 1
-        split = max(1, min(nkv, int(os.environ.get("BAM_CP_PULL_SPLIT", "1"))))
-
-        def pull(r, j):
+        def pull(r):
             def fn():
-                src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, self.kv_off[gi])
-                for h in range(j, nkv, split):
+                src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, 0)
+                for h in range(nkv):
                     k_all[h, r * rows:(r + 1) * rows].copy_(src[0, h])
                     v_all[h, r * rows:(r + 1) * rows].copy_(src[1, h])
                     _lib.call("bam_stream_write_i32", self.flags[r * nkv + h:].data_ptr(), epoch)
             return fn
-        peers = [(self.rank + step) % self.world for step in range(1, self.world)]
-        self._fan_out([pull(r, j) for j in range(split) for r in peers])
+        self._fan_out([pull((self.rank + step) % self.world) for step in range(1, self.world)])
         for t in (k_all, v_all):
             for st in self.streams:
                 t.record_stream(st)
@@ -260,48 +255,14 @@ class SymmExchange:
         self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
         return k_all, v_all, ev_local, ev_all, (self.flags, epoch)
 
-    def _gather_overlapped_token_major(self, gi, k_g, v_g):
-        nkv, rows, d = k_g.shape[1], self.rows, self.d
-        per = rows * nkv * d
-        mine = self.kv[self.kv_off[gi]:self.kv_off[gi] + 2 * per].view(2, rows, nkv, d)
-        mine[0, :k_g.shape[0]].copy_(k_g)
-        mine[1, :v_g.shape[0]].copy_(v_g)
-        k_all = torch.empty((self.world * rows, nkv, d), dtype=k_g.dtype, device=k_g.device)
-        v_all = torch.empty_like(k_all)
-        lo = self.rank * rows
-        k_all[lo:lo + k_g.shape[0]].copy_(k_g)
-        v_all[lo:lo + v_g.shape[0]].copy_(v_g)
-        self.kv_h.barrier(channel=0)
-        cur = torch.cuda.current_stream()
-        ev_local = torch.cuda.Event()
-        ev_local.record(cur)
-        if self.flags is None or self.flags.numel() < self.world:
-            self.flags = torch.zeros(self.world, dtype=torch.int32, device=k_g.device)
-        self.epoch += 1
-        epoch = self.epoch
-
-        def pull(r):
-            def fn():
-                src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, self.kv_off[gi])
-                k_all[r * rows:(r + 1) * rows].copy_(src[0])
-                v_all[r * rows:(r + 1) * rows].copy_(src[1])
-                _lib.call("bam_stream_write_i32", self.flags[r:].data_ptr(), epoch)
-            return fn
-        self._fan_out([pull((self.rank + s) % self.world) for s in range(1, self.world)])
-        for t in (k_all, v_all):
-            for st in self.streams:
-                t.record_stream(st)
-        ev_all = torch.cuda.Event()
-        ev_all.record(cur)
-        self.kv_h.barrier(channel=0)
-        return k_all, v_all, ev_local, ev_all, (self.flags, epoch)
-
-    def gather(self, gi: int, k_g: torch.Tensor, v_g: torch.Tensor):
-        """This rank's [n_local*128, nkv, d] K/V slice of head group gi ->
-        gathered rank-major [world*rows, nkv, d] K and V (the NCCL layout)."""
-        nkv, rows, d = k_g.shape[1], self.rows, self.d
-        per = rows * nkv * d
-        mine = self.kv[self.kv_off[gi]:self.kv_off[gi] + 2 * per].view(2, rows, nkv, d)
+    def gather(self, rows: int, kv0: int, k_g: torch.Tensor, v_g: torch.Tensor):
+        """This rank's [n_local*128, nkv, d] K/V slice of the KV heads
+        [kv0, kv0+nkv) -> gathered rank-major [world*rows, nkv, d] K and V
+        (the NCCL layout)."""
+        nkv, d = k_g.shape[1], self.d
+        self._check(rows, kv0, nkv)
+        off = 2 * rows * kv0 * d
+        mine = self.kv[off:off + 2 * rows * nkv * d].view(2, rows, nkv, d)
         mine[0, :k_g.shape[0]].copy_(k_g)
         mine[1, :v_g.shape[0]].copy_(v_g)
         k_all = torch.empty((self.world * rows, nkv, d), dtype=k_g.dtype, device=k_g.device)
@@ -310,7 +271,7 @@ class SymmExchange:
 
         def pull(r):
             def fn():
-                src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, self.kv_off[gi])
+                src = self.kv_h.get_buffer(r, (2, rows, nkv, d), torch.bfloat16, off)
                 k_all[r * rows:(r + 1) * rows].copy_(src[0])
                 v_all[r * rows:(r + 1) * rows].copy_(src[1])
             return fn
@@ -321,59 +282,30 @@ class SymmExchange:
         self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
         return k_all, v_all
 
-    def peer_slots(self, nkv: int) -> torch.Tensor:
+    def peer_slots(self, rows: int, nkv: int) -> torch.Tensor:
         """int64 device tensor: for every rank r, the UVA address of THIS rank's
-        slot [2][nkv][rows][d] fp32 in rank r's workspace (head group 0), which
-        the backward kernel's epilogue stores into directly (dkv_peers)."""
-        key = ("slots", nkv)
+        slot [2][nkv][rows][d] fp32 in rank r's workspace, which the backward
+        kernel's epilogue stores into directly (dkv_peers)."""
+        self._check(rows, 0, nkv)
+        key = ("slots", rows, nkv)
         t = self._cache.get(key)
         if t is None:
-            per = self.rows * nkv * self.d
-            base = self.ws_off[0] + self.rank * 2 * per
+            per = rows * nkv * self.d
+            base = self.rank * 2 * per
             ptrs = [self.ws_h.get_buffer(r, (2 * per,), torch.float32, base).data_ptr()
                     for r in range(self.world)]
             t = self._cache[key] = torch.tensor(ptrs, dtype=torch.int64, device=self.ws.device)
         return t
 
-    def reduce_direct(self, nkv: int, n_local: int):
+    def reduce_direct(self, rows: int, nkv: int, n_local: int):
         """Tail of the fused reduce-scatter: once every rank's backward kernel has
         stored its partials into the owners' workspaces (barrier), sum them into
         this rank's bf16 dK/dV."""
-        per = self.rows * nkv * self.d
+        per = rows * nkv * self.d
         self.ws_h.barrier(channel=0)          # every rank's kernel has finished its stores
-        out = self._reduce(self.ws_off[0], n_local, nkv, part=2 * per, comp=per,
-                           head=self.rows * self.d, row=self.d)
+        out = self._reduce(0, n_local, nkv, part=2 * per, comp=per, head=rows * self.d,
+                           row=self.d)
         self.ws_h.barrier(channel=0)          # summed before the next kernel stores
-        return out
-
-    def reduce_scatter_heads(self, dk_all, dv_all, n_local: int, head_done, ctas_per_head: int):
-        """reduce_scatter() for head-major partials [Hkv, world*rows, d] of one
-        head group that the backward kernel is STILL WRITING: every peer stream
-        waits (cuStreamWaitValue32, no SM) until head h's CTAs are done, then
-        pushes head h, so the transfer of heads 0..Hkv-2 overlaps the kernel.
-        Call with the current stream just before the kernel's launch point
-        ordered (the streams wait on an event recorded now)."""
-        Hkv, rows, d = dk_all.shape[0], self.rows, self.d
-        per = rows * Hkv * d
-        base = self.ws_off[0]
-
-        def push(r):
-            def fn():
-                dst = self.ws_h.get_buffer(r, (2, Hkv, rows, d), torch.float32,
-                                           base + self.rank * 2 * per)
-                for h in range(Hkv):
-                    _lib.call("bam_stream_wait_i32_geq", head_done[h:h + 1].data_ptr(),
-                              ctas_per_head)
-                    dst[0, h].copy_(dk_all[h, r * rows:(r + 1) * rows])
-                    dst[1, h].copy_(dv_all[h, r * rows:(r + 1) * rows])
-            return fn
-        self._fan_out([push((self.rank + step) % self.world) for step in range(self.world)])
-        for t in (dk_all, dv_all, head_done):
-            for st in self.streams:
-                t.record_stream(st)
-        self.ws_h.barrier(channel=0)          # every rank's partials have landed
-        out = self._reduce(base, n_local, Hkv, part=2 * per, comp=per, head=rows * d, row=d)
-        self.ws_h.barrier(channel=0)          # summed before the next pushes
         return out
 
     def _reduce(self, base, n_local, nkv, *, part, comp, head, row):
@@ -386,12 +318,15 @@ class SymmExchange:
                   nkv, n_local, dk.data_ptr(), dv.data_ptr())
         return dk, dv
 
-    def reduce_scatter(self, gi: int, dk_all: torch.Tensor, dv_all: torch.Tensor, n_local: int):
-        """fp32 partials [world*rows, nkv, d] of every key -> this rank's
-        summed [n_local*128, nkv, d] dK and dV."""
-        nkv, rows, d = dk_all.shape[1], self.rows, self.d
+    def reduce_scatter(self, rows: int, kv0: int, dk_all: torch.Tensor, dv_all: torch.Tensor,
+                       n_local: int):
+        """fp32 partials [world*rows, nkv, d] of every key (KV heads
+        [kv0, kv0+nkv)) -> this rank's summed [n_local*128, nkv, d] dK and dV."""
+        nkv, d = dk_all.shape[1], self.d
+        self._check(rows, kv0, nkv)
         per = rows * nkv * d
-        base = self.ws_off[gi]
+        base = self.world * 2 * rows * kv0 * d
+
         def push(r):
             def fn():
                 dst = self.ws_h.get_buffer(r, (2, rows, nkv, d), torch.float32,
@@ -409,6 +344,15 @@ class SymmExchange:
         return out
 
 
+def exchange_capacity(rows: int, nb: int, world: int) -> int:
+    """Padded rows per rank the exchange is allocated for: the plan's rows
+    plus 1/8 headroom, rounded up to 1024 tokens and capped at the whole
+    sequence, so the block counts of later masks (LPT moves a few blocks
+    between ranks) fit without a new rendezvous."""
+    cap = -(-(rows + rows // 8) // 1024) * 1024
+    return max(rows, min(cap, -(-nb * BLOCK // 1024) * 1024))
+
+
 @dataclass
 class CPPlan:
     layout: CPLayout
@@ -416,16 +360,26 @@ class CPPlan:
     assignment: B.DeviceAssignment
     policy: str
 
-    def exchange(self, head_groups, d, device, group=None) -> SymmExchange:
-        """The copy-engine transport for this plan's shapes.  The symmetric
-        buffers depend only on (world, rank, padded rows, head groups, d), so
-        plans of the same shape (a new mask every batch) share one exchange;
-        building one is a collective, reached in the same order on every rank."""
-        key = (self.layout.world, self.layout.rank, self.layout.max_blocks, tuple(head_groups), d,
-               str(device), id(group))
+    def exchange(self, hkv: int, d: int, device, group=None) -> SymmExchange:
+        """The copy-engine transport for this plan.  One exchange per (world,
+        rank, KV heads, d, device, group), allocated with headroom
+        (``exchange_capacity``) and reused by every later plan that fits, so
+        a new mask every batch does not rendezvous again; a plan that does
+        not fit replaces it (the old buffers are released after a device
+        sync and a barrier).  Every rank computes the identical plan, so all
+        ranks take the same branch (creating one is a collective)."""
+        lay = self.layout
+        rows = lay.max_blocks * BLOCK
+        key = (lay.world, lay.rank, hkv, d, str(device), id(group))
         ex = _EXCHANGES.get(key)
-        if ex is None:
-            ex = _EXCHANGES[key] = SymmExchange(self.layout, head_groups, d, device, group)
+        if ex is None or ex.cap_rows < rows:
+            if ex is not None:
+                torch.cuda.synchronize(device)
+                ex.kv_h.barrier(channel=0)
+                del _EXCHANGES[key]
+                del ex
+            cap = exchange_capacity(rows, self.attn.nb, lay.world)
+            ex = _EXCHANGES[key] = SymmExchange(cap, hkv, d, lay.world, lay.rank, device, group)
         return ex
 
     @property
@@ -486,54 +440,92 @@ def _head_groups(Hkv: int, groups: int):
     return [(g * per, per) for g in range(groups)]
 
 
-TRANSPORTS = ("nccl", "ce")
+TRANSPORTS = ("auto", "nccl", "ce")
+_TRANSPORT_CHOICE: dict = {}
+
+
+def resolve_transport(transport: str, plan: "CPPlan", hkv: int, d: int, device,
+                      group=None) -> str:
+    """"auto" (the default) -> "ce" when the symmetric-memory exchange can be
+    built on every rank, else "nccl".  The outcome is agreed collectively
+    (MIN over ranks of a success flag on the process group), so the ranks
+    never run different transports; it is decided once per group.  "auto"
+    at world 1 needs no exchange ("local"); a forced "nccl" / "ce" runs the
+    exchange even then (a one-rank process group)."""
+    if transport not in TRANSPORTS:
+        raise ValueError(f"transport must be one of {TRANSPORTS}")
+    if transport != "auto":
+        return transport
+    if plan.layout.world == 1:
+        return "local"
+    key = (id(group), str(device))
+    choice = _TRANSPORT_CHOICE.get(key)
+    if choice is None:
+        ok = 1
+        try:
+            plan.exchange(hkv, d, device, group)
+        except Exception:   # noqa: BLE001  (no peer mapping / symmetric memory on this box)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        choice = _TRANSPORT_CHOICE[key] = "ce" if int(flag.item()) == 1 else "nccl"
+    return choice
 
 
 def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups: int = 1,
-               transport: str = "nccl"):
-    """All-gather K/V per KV-head group on a side stream; the forward of group
-    g starts as soon as its K/V have landed, overlapping the gather of group
-    g+1 (the paper overlaps communication per head).
-    transport "nccl": NCCL all_gather; "ce": copy-engine pulls from symmetric
-    memory (SymmExchange).  Returns (o, lse, [(k_all_g, v_all_g)]); the
-    copy-engine overlap path's single group is head-major [Hkv, rows, d]
-    (``_kv_head_major`` tells the layouts apart)."""
-    if transport not in TRANSPORTS:
-        raise ValueError(f"transport must be one of {TRANSPORTS}")
+               transport: str = "auto", timer=None):
+    """K/V all-gather + the rank's attention forward.
+
+    transport "ce" (what "auto" picks when peer memory works): copy-engine
+    pulls from symmetric memory; for GQA with one head group the forward
+    starts on this rank's own key tiles at once and waits per tile on
+    per-(rank, KV head) arrival flags for the rest (no SM is spent on the
+    transfer, so the spin cannot starve it).  Otherwise (MHA, ``groups`` > 1
+    or "nccl") K/V travel per KV-head group on a side stream and the forward
+    of group g starts when its K/V have landed, overlapping the gather of
+    group g+1.
+
+    ``timer=(start, end)`` CUDA events recorded right around the forward
+    kernel launches (kernel-only time, no exchange barrier inside).
+    Returns (o, lse, [(k_all_g, v_all_g)]); the overlapped path's single
+    group is head-major [Hkv, rows, d] (``_kv_head_major`` tells them apart)."""
     Hq, Hkv = q_loc.shape[1], k_loc.shape[1]
     grp = Hq // Hkv
-    cur = torch.cuda.current_stream()
-    comm = _comm_stream(q_loc.device)
+    d = k_loc.shape[2]
+    transport = resolve_transport(transport, plan, Hkv, d, k_loc.device, group)
     o = torch.empty_like(q_loc)
     lse = torch.empty(Hq, q_loc.shape[0], dtype=torch.float32, device=q_loc.device)
+    if transport == "local":
+        A.attn_forward(q_loc, k_loc, v_loc, plan.attn, scale, out=(o, lse), timer=timer)
+        return o, lse, [(k_loc, v_loc)]
+    cur = torch.cuda.current_stream()
+    comm = _comm_stream(q_loc.device)
+    rows = plan.layout.max_blocks * BLOCK
     gathered, events = [], []
     hg = _head_groups(Hkv, groups)
-    ex = plan.exchange(hg, k_loc.shape[2], k_loc.device, group) if transport == "ce" else None
-    if (ex is not None and len(hg) == 1 and grp % 2 == 0
-            and os.environ.get("BAM_CP_OVERLAP", "1") != "0"
-            and os.environ.get("BAM_FWD_2CTA", "0") != "1"):
-        # the forward starts on this rank's key tiles while the copy engines pull the
-        # peers' K/V; its tiles of other ranks wait on per-rank arrival flags.  GQA only:
-        # for MHA (query-block pairs, whose union lists are not local-first) it measured
-        # slower than gathering first (config 2, N=4: 3269 vs 3395 TFLOP/s)
-        head_major = os.environ.get("BAM_CP_KV_HEAD_MAJOR", "1") != "0"
+    ex = plan.exchange(Hkv, d, k_loc.device, group) if transport == "ce" else None
+    if ex is not None and len(hg) == 1 and grp % 2 == 0:
+        # GQA: the forward starts on this rank's key tiles while the copy engines pull the
+        # peers' K/V.  MHA runs query-block pairs whose union lists are not local-first; it
+        # measured slower than gathering first (config 2, N=4: 3269 vs 3395 TFLOP/s)
         comm.wait_stream(cur)
         with torch.cuda.stream(comm):
             k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(
-                0, k_loc, v_loc, head_major)
+                rows, k_loc, v_loc)
         cur.wait_event(ev_local)
         k_all.record_stream(cur)
         v_all.record_stream(cur)
         A.attn_forward(q_loc, k_all, v_all, plan.attn, scale, out=(o, lse),
                        kv_ready=(flags, epoch, plan.layout.rank, plan.layout.max_blocks),
-                       kv_head_major=head_major)
+                       kv_head_major=True, timer=timer)
         cur.wait_event(ev_all)
         return o, lse, [(k_all, v_all)]
     comm.wait_stream(cur)
     with torch.cuda.stream(comm):
-        for gi, (kv0, nkv) in enumerate(hg):
+        for kv0, nkv in hg:
             if ex is not None:
-                k_all, v_all = ex.gather(gi, k_loc[:, kv0:kv0 + nkv], v_loc[:, kv0:kv0 + nkv])
+                k_all, v_all = ex.gather(rows, kv0, k_loc[:, kv0:kv0 + nkv],
+                                         v_loc[:, kv0:kv0 + nkv])
             else:
                 kg = k_loc[:, kv0:kv0 + nkv].contiguous()
                 vg = v_loc[:, kv0:kv0 + nkv].contiguous()
@@ -542,12 +534,16 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
             ev.record(comm)
             gathered.append((k_all, v_all))
             events.append(ev)
-    for (kv0, nkv), (k_all, v_all), ev in zip(_head_groups(Hkv, groups), gathered, events):
+    for i, ((kv0, nkv), (k_all, v_all), ev) in enumerate(zip(hg, gathered, events)):
         cur.wait_event(ev)
         k_all.record_stream(cur)
         v_all.record_stream(cur)
+        if timer is not None and i == 0:
+            timer[0].record()
         A.attn_forward(q_loc, k_all, v_all, plan.attn, scale, h_begin=kv0 * grp, nh=nkv * grp,
                        out=(o, lse))
+    if timer is not None:
+        timer[1].record()
     return o, lse, gathered
 
 
@@ -558,60 +554,45 @@ def _kv_head_major(k_all, plan: CPPlan) -> bool:
 
 
 def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=None,
-                timers=None, transport: str = "nccl"):
-    """Per KV-head group: backward kernel -> fp32 dK/dV partials of every key,
-    reduce-scattered on the side stream while the next group computes."""
+                timers=None, transport: str = "auto"):
+    """The rank's backward: dQ of its query rows and the fp32 dK/dV partials
+    of every key, reduce-scattered to the key owners.
+
+    "ce" with one head group: the reduce-scatter is fused into the backward
+    kernel's epilogue (each CTA stores its partial rows straight into the
+    owner's symmetric workspace), then one barrier and a local sum.
+    Otherwise, per KV-head group: backward kernel, then the reduce-scatter of
+    that group on the side stream while the next group computes.
+    ``timers[i] = (start, end)``: events around head group i's main kernel."""
     Hq = q_loc.shape[1]
     kvh = [_kv_head_major(k, plan) for k, _ in gathered]
     if any(kvh) and len(gathered) != 1:
         raise ValueError("head-major gathered K/V come as one head group")
     Hkv = sum(k.shape[0] if h else k.shape[1] for (k, _), h in zip(gathered, kvh))
     grp = Hq // Hkv
+    d = q_loc.shape[2]
+    transport = resolve_transport(transport, plan, Hkv, d, q_loc.device, group)
+    ws = A.BackwardWorkspace(q_loc, o, lse, do, plan.attn, scale)
+    if transport == "local":
+        k_all, v_all = gathered[0]
+        dk, dv = ws.main(k_all, v_all, timer=None if timers is None else timers[0])
+        return ws.finalize(), A.to_bf16(dk), A.to_bf16(dv)
     cur = torch.cuda.current_stream()
     comm = _comm_stream(q_loc.device)
-    ws = A.BackwardWorkspace(q_loc, o, lse, do, plan.attn, scale)
-    if kvh[0]:
-        hg = [(0, Hkv)]
-    else:
-        hg = [(sum(k.shape[1] for k, _ in gathered[:i]), k.shape[1]) for i, (k, _) in
-              enumerate(gathered)]
-    ex = plan.exchange(hg, q_loc.shape[2], q_loc.device, group) if transport == "ce" else None
+    rows = plan.layout.max_blocks * BLOCK
+    n_loc_rows = plan.layout.n_local * BLOCK
+    ex = plan.exchange(Hkv, d, q_loc.device, group) if transport == "ce" else None
     if kvh[0] and ex is None:
         raise ValueError("head-major gathered K/V need the copy-engine transport")
-    if (ex is not None and len(gathered) == 1
-            and os.environ.get("BAM_CP_RS_DIRECT", "1") != "0"):
-        # reduce-scatter fused into the backward epilogue: each CTA stores its fp32
-        # dK/dV partial rows straight into the key owner's symmetric workspace
-        # (NVLink stores); after the kernel only a barrier and the local sum remain
+    if ex is not None and len(gathered) == 1:
         k_all, v_all = gathered[0]
-        ws.main(k_all, v_all, kv_head_major=kvh[0], dkv_peers=ex.peer_slots(Hkv),
-                rows_per_owner=ex.rows, timer=None if timers is None else timers[0])
+        ws.main(k_all, v_all, kv_head_major=kvh[0], dkv_peers=ex.peer_slots(rows, Hkv),
+                rows_per_owner=rows, timer=None if timers is None else timers[0])
         done = torch.cuda.Event()
         done.record(cur)
         with torch.cuda.stream(comm):
             comm.wait_event(done)
-            dk, dv = ex.reduce_direct(Hkv, plan.layout.n_local * BLOCK)
-        dq = ws.finalize()
-        cur.wait_stream(comm)
-        dk.record_stream(cur)          # allocated on the comm stream
-        dv.record_stream(cur)
-        return dq, dk, dv
-    if (ex is not None and len(gathered) == 1
-            and (kvh[0] or os.environ.get("BAM_CP_RS_OVERLAP", "1") != "0")):
-        # the copy engines ship each KV head's dK/dV partials as soon as the
-        # backward kernel's CTAs of that head have finished (per-head counters)
-        k_all, v_all = gathered[0]
-        head_done = torch.zeros(Hkv, dtype=torch.int32, device=q_loc.device)
-        ready = torch.cuda.Event()
-        ready.record(cur)
-        dk_all, dv_all = ws.main(k_all, v_all, head_done=head_done, head_major=True,
-                                 kv_head_major=kvh[0],
-                                 timer=None if timers is None else timers[0])
-        with torch.cuda.stream(comm):
-            comm.wait_event(ready)
-            head_done.record_stream(comm)
-            dk, dv = ex.reduce_scatter_heads(dk_all, dv_all, plan.layout.n_local * BLOCK,
-                                             head_done, ws.ctas_per_head())
+            dk, dv = ex.reduce_direct(rows, Hkv, n_loc_rows)
         dq = ws.finalize()
         cur.wait_stream(comm)
         dk.record_stream(cur)          # allocated on the comm stream
@@ -628,7 +609,7 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
             comm.wait_event(ev)
             dk_all.record_stream(comm)
             dv_all.record_stream(comm)
-            parts.append(ex.reduce_scatter(i, dk_all, dv_all, plan.layout.n_local * BLOCK)
+            parts.append(ex.reduce_scatter(rows, kv0, dk_all, dv_all, n_loc_rows)
                          if ex is not None else
                          scatter_dkv(dk_all, dv_all, plan.layout, group))
         kv0 += nkv
@@ -662,9 +643,13 @@ class _CPAttention(torch.autograd.Function):
 
 
 def cp_bitfield_attention(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None,
-                          groups: int = 1, transport: str = "nccl"):
+                          groups: int = 1, transport: str = "auto"):
     """Context-parallel bitfield attention with autograd.  Inputs are this
-    rank's rows (``shard_rows``) of q/k/v; returns this rank's O rows.  K/V
-    travel in ``groups`` KV-head groups so communication overlaps compute,
-    over NCCL (``transport="nccl"``) or the copy engines (``"ce"``)."""
+    rank's rows (``shard_rows``) of q/k/v; returns this rank's O rows.
+
+    ``transport``: "auto" (default) uses the copy-engine exchange over
+    NVLink peer memory -- the forward overlaps the K/V pulls, the
+    reduce-scatter is fused into the backward -- and falls back to NCCL
+    collectively when peer memory is unavailable; "nccl" / "ce" force one.
+    ``groups`` > 1 pipelines the exchange per KV-head group."""
     return _CPAttention.apply(q_loc, k_loc, v_loc, plan, group, scale, groups, transport)

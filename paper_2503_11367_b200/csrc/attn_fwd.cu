@@ -970,6 +970,17 @@ __global__ void __launch_bounds__(128) combine_kernel(const BamAttnFwdParams p,
 
 using namespace bam;
 
+// CP-overlap flags: ``ready`` is a 64-bit per-rank mask in the kernels and the owner
+// of a block-row is k_row / kv_rows_per_rank (validate both on the host)
+#define BAM_CHECK_KV_READY(p, fn)                                                          \
+  BAM_CHECK_ARG(!(p).kv_ready ||                                                           \
+                    ((p).kv_rows_per_rank >= 1 &&                                          \
+                     ((p).k_rows + (p).kv_rows_per_rank - 1) / (p).kv_rows_per_rank <= 64 && \
+                     (p).kv_rank >= 0 && (p).kv_rank < 64),                                \
+                fn ": kv_ready needs kv_rows_per_rank >= 1 and at most 64 ranks "          \
+                   "(kv_rows_per_rank=%d k_rows=%d kv_rank=%d)",                           \
+                (p).kv_rows_per_rank, (p).k_rows, (p).kv_rank)
+
 extern "C" int bam_attn_fwd_combine(const BamAttnFwdParams* pp, const int32_t* combine,
                                     int32_t n_combine, void* stream) {
   BAM_CHECK_ARG(pp != nullptr && combine != nullptr && n_combine >= 0,
@@ -993,6 +1004,8 @@ extern "C" int bam_attn_fwd(const BamAttnFwdParams* pp, void* stream) {
                 "bam_attn_fwd: head group [%d, %d) of Hq=%d over Hkv=%d", p.h_begin,
                 p.h_begin + nh, p.Hq, p.Hkv);
   BAM_CHECK_ARG(p.nq <= 65535, "bam_attn_fwd: nq=%d > 65535", p.nq);
+  BAM_CHECK_KV_READY(p, "bam_attn_fwd");
+  BAM_CHECK_ARG(!p.kv_ready || !p.part_o, "bam_attn_fwd: kv_ready needs whole rows");
   CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_tmap_rows_heads_d128(&mq, p.q, (int64_t)p.nq * 128, p.Hq, 128))) return rc;
@@ -1034,6 +1047,7 @@ extern "C" int bam_attn_fwd_2cta(const BamAttnFwdParams* pp, const int32_t* pair
                     (nh / p.Hkv) % 2 == 0 && p.h_begin >= 0 && p.h_begin + nh <= p.Hq,
                 "bam_attn_fwd_2cta: needs an even GQA group (nh=%d Hkv=%d)", nh, p.Hkv);
   BAM_CHECK_ARG(n_pairs >= 0, "bam_attn_fwd_2cta: n_pairs=%d", n_pairs);
+  BAM_CHECK_ARG(!p.kv_ready, "bam_attn_fwd_2cta: the CTA-pair kernel does not wait on kv_ready");
   if (n_pairs == 0) return kOk;
   CUtensorMap mq, mk64, mv;
   int rc;
@@ -1077,6 +1091,7 @@ extern "C" int bam_attn_fwd_qpairs(const BamAttnFwdParams* pp, const int32_t* pa
                 "bam_attn_fwd_qpairs: head group [%d, %d) of Hq=%d over Hkv=%d", p.h_begin,
                 p.h_begin + nh, p.Hq, p.Hkv);
   BAM_CHECK_ARG(n_pairs >= 0, "bam_attn_fwd_qpairs: n_pairs=%d", n_pairs);
+  BAM_CHECK_KV_READY(p, "bam_attn_fwd_qpairs");
   if (n_pairs == 0) return kOk;
   CUtensorMap mq, mk, mv;
   int rc;

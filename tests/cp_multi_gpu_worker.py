@@ -1,0 +1,151 @@
+#!/usr/bin/env python3
+"""Multi-GPU parity worker for tests/test_gpu_multi.py (one process per GPU).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/cp_multi_gpu_worker.py \
+        --transport {auto,nccl,ce} [--config 4] [--policy lpt]
+
+Every rank runs ``cp_bitfield_attention`` forward + backward (autograd, the
+drop-in API) on its assigned query blocks of the full-size BASELINE.json
+config (default 4: 128K EMU multi-image mask, GQA 32q/8kv), twice (the second
+step reuses the exchange buffers), and checks ITS OWN rows:
+
+* O and dQ of sampled local query blocks (first, heaviest, last) against the
+  fp32 CPU oracle (those rows against all keys);
+* dK/dV of the last key block if this rank owns it (only the last query
+  block sees it, so the oracle is cheap) against the oracle;
+* every local row of O/dQ and every owned row of dK/dV against the
+  single-GPU path (``bitfield_attention`` on the whole sequence, itself
+  oracle-checked at this size by tests/test_gpu_large.py) -- the exchange
+  must not change results beyond fp32 summation order.
+
+Tolerance: max-abs 2e-2 and relative-L2 1e-2 (bf16 kernel vs fp32 oracle);
+for the bf16 dK/dV the API returns, the max-abs check discounts the output
+rounding itself (2^-7 |x|, two roundings apart).
+Rank 0 prints one JSON line; the exit code is non-zero on any failure.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import attention_ref  # noqa: E402
+from paper_2503_11367_b200 import attention as A, cp, mask as M  # noqa: E402
+from paper_2503_11367_b200.workloads import CONFIGS  # noqa: E402
+
+MAX_ABS, REL_L2 = 2e-2, 1e-2
+
+
+def err(got, ref, bf16_out=False):
+    """(max-abs, rel-L2).  ``bf16_out``: the API returns dK/dV rounded to
+    bf16, whose own rounding is up to 2^-8 |x| (2^-7 between two roundings):
+    that much is discounted from each element's error before the max."""
+    got, ref = got.float().cpu(), ref.float().cpu()
+    d = (got - ref).abs()
+    if bf16_out:
+        d = (d - ref.abs() * 2.0 ** -7).clamp_min(0)
+    return d.max().item(), ((got - ref).norm() / ref.norm().clamp_min(1e-12)).item()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--transport", default="auto")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--policy", default="lpt")
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    torch.set_num_threads(max(1, len(os.sched_getaffinity(0)) // world))
+
+    cfg = CONFIGS[args.config]
+    Hq, Hkv = cfg["Hq"], cfg["Hkv"]
+    mask = M.build_bitfield(cfg["segments"])
+    desc_d = mask.device_descriptors()
+    T = desc_d.shape[0]
+    nb = T // 128
+    desc = desc_d.cpu().numpy()
+    plan = cp.make_cp_plan(mask, world, rank, args.policy)
+    lay = plan.layout
+    transport = cp.resolve_transport(args.transport, plan, Hkv, 128, dev)
+
+    g = torch.Generator().manual_seed(1234)
+    q, k, v, do = (torch.randn(T, h, 128, generator=g).to(torch.bfloat16)
+                   for h in (Hq, Hkv, Hkv, Hq))
+    qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
+    q_loc, k_loc, v_loc, do_loc = cp.shard_rows(qd, kd, vd, dod, layout=lay)
+    leaves = [t.clone().requires_grad_(True) for t in (q_loc, k_loc, v_loc)]
+    for _ in range(2):
+        for t in leaves:
+            t.grad = None
+        o = cp.cp_bitfield_attention(*leaves, plan, transport=transport)
+        o.backward(do_loc)
+    torch.cuda.synchronize()
+    o_loc, dq_loc, dk_loc, dv_loc = (o.detach(), leaves[0].grad, leaves[1].grad, leaves[2].grad)
+
+    checks = {}
+
+    def record(name, got, ref):
+        ma, rl = err(got, ref, bf16_out=name[:2] in ("dK", "dV"))
+        checks[name] = {"max_abs": ma, "rel_l2": rl, "ok": ma <= MAX_ABS and rl <= REL_L2}
+
+    # (1) oracle on sampled local query blocks
+    local = lay.local_blocks.cpu().numpy()
+    W = plan.attn.W.cpu().numpy()
+    picks = sorted({0, int(np.argmax(W[local])), len(local) - 1})
+    rows_loc = np.concatenate([np.arange(i * 128, (i + 1) * 128) for i in picks])
+    rows_glb = np.concatenate([np.arange(local[i] * 128, (local[i] + 1) * 128) for i in picks])
+    rg = torch.from_numpy(rows_glb)
+    o_ref, lse_ref = attention_ref.attention_fwd(q[rg], k, v, desc, rows_glb, chunk=128)
+    dq_ref, _, _ = attention_ref.attention_bwd(q[rg], k, v, o_ref, lse_ref, do[rg], desc,
+                                               rows_glb, chunk=128)
+    rl = torch.from_numpy(rows_loc).to(dev)
+    record("O_oracle_sampled", o_loc[rl], o_ref)
+    record("dQ_oracle_sampled", dq_loc[rl], dq_ref)
+
+    # (2) oracle dK/dV of the last key block (seen by the last query block only)
+    pos = np.nonzero(local == nb - 1)[0]
+    if pos.size:
+        i = int(pos[0])
+        rows = np.arange((nb - 1) * 128, nb * 128)
+        rt = torch.from_numpy(rows)
+        o_r, lse_r = attention_ref.attention_fwd(q[rt], k, v, desc, rows, chunk=128)
+        _, dk_r, dv_r = attention_ref.attention_bwd(q[rt], k, v, o_r, lse_r, do[rt], desc, rows,
+                                                    chunk=128)
+        record("dK_oracle_last_block", dk_loc[i * 128:(i + 1) * 128], dk_r[rt])
+        record("dV_oracle_last_block", dv_loc[i * 128:(i + 1) * 128], dv_r[rt])
+
+    # (3) every local / owned row against the single-GPU path
+    full = [t.clone().requires_grad_(True) for t in (qd, kd, vd)]
+    of = A.bitfield_attention(*full, A.plan_for_mask(mask))
+    of.backward(dod)
+    rows_all = (lay.local_blocks.long()[:, None] * 128 +
+                torch.arange(128, device=dev)).reshape(-1)
+    record("O_vs_single_gpu", o_loc, of.detach()[rows_all])
+    record("dQ_vs_single_gpu", dq_loc, full[0].grad[rows_all])
+    record("dK_vs_single_gpu", dk_loc, full[1].grad[rows_all])
+    record("dV_vs_single_gpu", dv_loc, full[2].grad[rows_all])
+
+    ok = torch.tensor([int(all(c["ok"] for c in checks.values()))], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    reports = [None] * world
+    dist.all_gather_object(reports, {"rank": rank, "n_local": lay.n_local, **checks})
+    if rank == 0:
+        print(json.dumps({"world": world, "config": cfg["name"], "policy": args.policy,
+                          "transport": transport, "ok": bool(ok.item()),
+                          "imbalance_predicted": plan.predicted_imbalance,
+                          "ranks": reports}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok.item() else 1)
+
+
+if __name__ == "__main__":
+    main()

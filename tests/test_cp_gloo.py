@@ -31,6 +31,7 @@ def _worker(rank, world, port, policy, result_dir):
     from oracle import attention_ref, balance_ref, mask_ref
     from paper_2503_11367_b200 import cp
 
+    torch.set_num_threads(1)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -111,6 +112,16 @@ def test_cp_exchange_zigzag(tmp_path):
 def test_cp_exchange_lpt_world4(tmp_path):
     # uneven per-rank block counts and padded shards across four ranks
     _run("lpt", tmp_path, world=4)
+
+
+def test_cp_exchange_lpt_world8(tmp_path):
+    # the north-star CP degree: eight ranks, 10 blocks -> some ranks own one block
+    _run("lpt", tmp_path, world=8)
+
+
+def test_cp_exchange_zigzag_world8(tmp_path):
+    # zigzag with 2G = 16 chunks over 10 blocks: empty chunks, ranks without blocks
+    _run("zigzag", tmp_path, world=8)
 
 
 def test_cp_layout_unequal_counts():

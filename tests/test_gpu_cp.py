@@ -251,3 +251,99 @@ def test_forward_waits_on_kv_arrival_flags():
     o, lse = A.attn_forward(q, k2, v2, plan, kv_ready=(flags, 7, 0, nb // 2))
     torch.cuda.synchronize()
     assert torch.equal(o, o_ref) and torch.equal(lse, lse_ref)
+
+
+def test_cp_emulated_world8_config4_overlapped_forward():
+    """The north-star shape at CP=8 with the copy-engine layout, ranks emulated
+    one after another on one GPU: config 4 (128K EMU multi-image, GQA 32q/8kv),
+    head-major gathered K/V [Hkv, 8*rows, d] whose peers' rows land on a side
+    stream AFTER the forward starts, signalled through the world*Hkv = 64
+    arrival flags (bam_stream_write_i32) that the kernel waits on per tile.
+    Per rank: O/dQ of every local row against the single-GPU path (itself
+    oracle-checked at this size in tests/test_gpu_large.py), the heaviest local
+    query block against the fp32 oracle, and the dK/dV partials of all eight
+    ranks summed against the single-GPU fp32 dK/dV."""
+    from paper_2503_11367_b200 import _lib
+    from paper_2503_11367_b200 import attention as A
+    from paper_2503_11367_b200 import cp
+    from paper_2503_11367_b200 import mask as M
+    from paper_2503_11367_b200.workloads import CONFIGS
+
+    world, cfg = 8, CONFIGS[4]
+    Hq, Hkv = cfg["Hq"], cfg["Hkv"]
+    mask = M.build_bitfield(cfg["segments"])
+    d_desc = mask.device_descriptors()
+    T = d_desc.shape[0]
+    desc = d_desc.cpu().numpy()
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(1234)
+    q, k, v, do = (torch.randn(T, h, 128, generator=g).to(torch.bfloat16)
+                   for h in (Hq, Hkv, Hkv, Hq))
+    qd, kd, vd, dod = (t.to(dev) for t in (q, k, v, do))
+    full = A.plan_for_mask(mask)
+    o_1, lse_1 = A.attn_forward(qd, kd, vd, full)
+    dq_1, dk_1, dv_1 = A.attn_backward(qd, kd, vd, o_1, lse_1, dod, full, dkv_fp32=True)
+    dk_sum = torch.zeros(T, Hkv, 128, device=dev)
+    dv_sum = torch.zeros_like(dk_sum)
+    side = torch.cuda.Stream()
+    for rank in range(world):
+        plan = cp.make_cp_plan(d_desc, world, rank, "lpt")
+        lay = plan.layout
+        rows = lay.max_blocks * BLOCK
+        idx = (lay.k_row.to(torch.int64)[:, None] * BLOCK +
+               torch.arange(BLOCK, device=dev)[None, :]).reshape(-1)
+        k_all = torch.zeros(Hkv, world * rows, 128, dtype=torch.bfloat16, device=dev)
+        v_all = torch.zeros_like(k_all)
+        mine = torch.zeros(world * rows, dtype=torch.bool, device=dev)
+        mine[rank * rows:(rank + 1) * rows] = True
+        k_src = torch.zeros_like(k_all)
+        v_src = torch.zeros_like(v_all)
+        k_src[:, idx] = kd.transpose(0, 1)
+        v_src[:, idx] = vd.transpose(0, 1)
+        k_all[:, mine] = k_src[:, mine]          # this rank's rows: present at launch
+        v_all[:, mine] = v_src[:, mine]
+        flags = torch.zeros(world * Hkv, dtype=torch.int32, device=dev)
+        epoch = 3 + rank
+        q_loc, do_loc = cp.shard_rows(qd, dod, layout=lay)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(20_000_000)        # the peers' rows land after the launch
+            for peer in range(world):
+                if peer == rank:
+                    continue
+                sl = slice(peer * rows, (peer + 1) * rows)
+                for h in range(Hkv):
+                    k_all[h, sl].copy_(k_src[h, sl])
+                    v_all[h, sl].copy_(v_src[h, sl])
+                    _lib.call("bam_stream_write_i32", flags[peer * Hkv + h:].data_ptr(), epoch)
+        o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn,
+                                kv_ready=(flags, epoch, rank, lay.max_blocks), kv_head_major=True)
+        torch.cuda.synchronize()
+        assert int(flags.min().item()) in (0, epoch)
+        ws = A.BackwardWorkspace(q_loc, o, lse, do_loc, plan.attn, None)
+        dk_all, dv_all = ws.main(k_all, v_all, kv_head_major=True)
+        dq = ws.finalize()
+        dk_sum += dk_all[idx]
+        dv_sum += dv_all[idx]
+        pos = (lay.local_blocks.to(torch.int64)[:, None] * BLOCK +
+               torch.arange(BLOCK, device=dev)[None, :]).reshape(-1)
+        assert (o.float() - o_1[pos].float()).abs().max().item() < 2e-2, rank
+        assert rel_l2(o, o_1[pos]) < 1e-2
+        d = (dq.float() - dq_1[pos].float()).abs() - dq_1[pos].float().abs() * 2.0 ** -7
+        assert d.max().item() < 2e-2 and rel_l2(dq, dq_1[pos]) < 1e-2, rank
+        # the heaviest local query block against the oracle
+        W = plan.attn.W[lay.local_blocks.long()]
+        i = int(torch.argmax(W).item())
+        b = int(lay.local_blocks[i].item())
+        rws = np.arange(b * BLOCK, (b + 1) * BLOCK)
+        rt = torch.from_numpy(rws)
+        o_ref, lse_ref = attention_ref.attention_fwd(q[rt], k, v, desc, rws, chunk=128)
+        dq_ref, _, _ = attention_ref.attention_bwd(q[rt], k, v, o_ref, lse_ref, do[rt], desc, rws,
+                                                   chunk=128)
+        sl = slice(i * BLOCK, (i + 1) * BLOCK)
+        assert (o[sl].float().cpu() - o_ref).abs().max().item() < 2e-2
+        assert (lse[:, sl].cpu() - lse_ref).abs().max().item() < 2e-3
+        assert (dq[sl].float().cpu() - dq_ref).abs().max().item() < 2e-2
+        assert rel_l2(dq[sl], dq_ref) < 1e-2
+    assert rel_l2(dk_sum, dk_1) < 1e-2 and (dk_sum - dk_1).abs().max().item() < 2e-2
+    assert rel_l2(dv_sum, dv_1) < 1e-2 and (dv_sum - dv_1).abs().max().item() < 2e-2

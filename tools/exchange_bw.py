@@ -8,8 +8,7 @@ K/V all-gather and the backward dK/dV reduce-scatter of the padded config-4
 shards, through both transports: "nccl" (cp.gather_kv / cp.scatter_dkv) and
 "ce" (cp.SymmExchange copy-engine pulls / pushes over torch symmetric
 memory, its device barriers included), plus "ce_head_major" = the
-gather_overlapped() pulls bench.py uses (BAM_CP_PULL_SPLIT copy streams per
-peer).  Prints one JSON line per
+gather_overlapped() pulls bench.py uses (one copy stream per peer).  Prints one JSON line per
 (step, transport): peer bytes per rank (what crosses NVLink into, for the
 gather, or out of, for the reduce-scatter, one GPU) and that over the time.
 """
@@ -44,18 +43,18 @@ k_loc = torch.randn(n_loc, Hkv, D, device=dev, generator=g, dtype=torch.bfloat16
 v_loc = torch.randn_like(k_loc)
 dk_all = torch.randn(world * rows, Hkv, D, device=dev, generator=g, dtype=torch.float32)
 dv_all = torch.randn_like(dk_all)
-ex = plan.exchange(cp._head_groups(Hkv, 1), D, dev)
+ex = plan.exchange(Hkv, D, dev)
 
 gather_bytes = (world - 1) * rows * Hkv * D * 2 * 2          # bf16 K and V from every peer
 rs_bytes = (world - 1) * rows * Hkv * D * 4 * 2              # fp32 dK and dV to every peer
 
 steps = {
     ("kv_all_gather", "nccl"): (lambda: cp.gather_kv(k_loc, v_loc, lay), gather_bytes),
-    ("kv_all_gather", "ce"): (lambda: ex.gather(0, k_loc, v_loc), gather_bytes),
-    ("kv_all_gather", "ce_head_major"): (lambda: ex.gather_overlapped(0, k_loc, v_loc),
+    ("kv_all_gather", "ce"): (lambda: ex.gather(rows, 0, k_loc, v_loc), gather_bytes),
+    ("kv_all_gather", "ce_head_major"): (lambda: ex.gather_overlapped(rows, k_loc, v_loc),
                                          gather_bytes),
     ("dkv_reduce_scatter", "nccl"): (lambda: cp.scatter_dkv(dk_all, dv_all, lay), rs_bytes),
-    ("dkv_reduce_scatter", "ce"): (lambda: ex.reduce_scatter(0, dk_all, dv_all, n_loc),
+    ("dkv_reduce_scatter", "ce"): (lambda: ex.reduce_scatter(rows, 0, dk_all, dv_all, n_loc),
                                    rs_bytes),
 }
 
@@ -80,7 +79,6 @@ for (name, transport), (fn, nbytes) in steps.items():
     ms = ms.item()
     if rank == 0:
         print(json.dumps({"step": name, "transport": transport, "n_gpus": world,
-                          "pull_split": int(os.environ.get("BAM_CP_PULL_SPLIT", "1")),
                           "workload": "config4_emu_multi_image_128k", "rows_per_rank": rows,
                           "peer_bytes_per_rank": nbytes, "ms": ms,
                           "nvlink_gbs_per_rank": nbytes / ms / 1e6}), flush=True)
