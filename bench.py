@@ -141,8 +141,10 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU arm
 def cpu_attention_sample(segments, Hq, Hkv, blocks, seed=1234):
-    """fp32 oracle fwd+bwd for `blocks` query blocks (all heads) against all
-    keys; returns (seconds, masked FLOP, sample description)."""
+    """fp32 oracle fwd+bwd for `blocks` query blocks (all heads), each against
+    the keys of its non-skip tiles only (blockwise-sparse, PAPER.md:616-619:
+    skipped tiles are never computed, as on the GPU); returns (seconds,
+    masked FLOP, sample description)."""
     import numpy as np
     import torch
 
@@ -151,6 +153,7 @@ def cpu_attention_sample(segments, Hq, Hkv, blocks, seed=1234):
     desc, _ = mask_ref.build_bitfield(segments)
     desc = np.asarray(desc, np.int64)
     T = desc.shape[0]
+    classes, _ = mask_ref.block_workloads_c(desc, 128)
     g = torch.Generator().manual_seed(seed)
     k = torch.randn(T, Hkv, D, generator=g)
     v = torch.randn(T, Hkv, D, generator=g)
@@ -158,11 +161,18 @@ def cpu_attention_sample(segments, Hq, Hkv, blocks, seed=1234):
     q = torch.randn(len(rows), Hq, D, generator=g)
     do = torch.randn(len(rows), Hq, D, generator=g)
     n_allowed = mask_ref.count_allowed_rows(desc, rows)
+    keys = [np.concatenate([np.arange(kb * 128, (kb + 1) * 128)
+                            for kb in np.nonzero(classes[b])[0]]) for b in blocks]
     t0 = time.perf_counter()
-    o, lse = attention_ref.attention_fwd(q, k, v, desc, rows)
-    attention_ref.attention_bwd(q, k, v, o, lse, do, desc, rows)
+    for i, b in enumerate(blocks):
+        sl = slice(i * 128, (i + 1) * 128)
+        kp = torch.from_numpy(keys[i])
+        ks, vs = k[kp], v[kp]
+        o, lse = attention_ref.attention_fwd(q[sl], ks, vs, desc, rows[sl], k_pos=keys[i])
+        attention_ref.attention_bwd(q[sl], ks, vs, o, lse, do[sl], desc, rows[sl], k_pos=keys[i])
     dt = time.perf_counter() - t0
-    return dt, 14.0 * D * Hq * n_allowed, f"{len(blocks)} query block(s) {list(blocks)} x {Hq} heads vs all {T} keys"
+    return dt, 14.0 * D * Hq * n_allowed, (f"{len(blocks)} query block(s) {list(blocks)} x {Hq} "
+                                           f"heads vs the keys of their non-skip tiles")
 
 
 def sample_blocks(nb, count, step=0):
@@ -181,6 +191,7 @@ def run_reference(args, cfg, rank, world):
     nb = sum(c for _, c in cfg["segments"]) // 128
     for w in range(args.warmup):
         cpu_attention_sample(cfg["segments"], cfg["Hq"], cfg["Hkv"], sample_blocks(nb, 1, w))
+    planning = cpu_planning_sample(cfg["segments"], max(world, cfg["cp"]))
     times, flops = [], []
     for s in range(args.steps):
         dt, fl, sample = cpu_attention_sample(cfg["segments"], cfg["Hq"], cfg["Hkv"],
@@ -197,13 +208,95 @@ def run_reference(args, cfg, rank, world):
         "config": {"workload": cfg["name"], "tokens": nb * 128, "Hq": cfg["Hq"],
                    "Hkv": cfg["Hkv"], "head_dim": D, "cp": world},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-                         "sample": "per step: 1 query block x all heads vs all keys, fp32 "
-                                   "oracle fwd+bwd (oracle/attention_ref.py; the reference "
-                                   "has no attention code)"},
+                         "sample": "per step: 1 query block x all heads vs the keys of its "
+                                   "non-skip tiles, fp32 oracle fwd+bwd (oracle/attention_ref.py; "
+                                   "the reference has no attention code)",
+                         "planning": planning},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     emit(line)
+
+
+# --------------------------------------------------------------------------- planning
+def time_planning(M, CP, B, A, cfg, world, rank, policy, plan, reps=5):
+    """The planning stage on the GPU (north-star subsystem 2): K1 block
+    summaries + K2 tile classes / W (classify_device), K3 the block
+    assignment, and the per-rank planner (bam_plan_build), each timed with
+    CUDA events on the current stream (median of ``reps``); plus the
+    wall-clock of the whole public call chain build_bitfield + make_cp_plan
+    (its one host sync included)."""
+    import torch
+
+    mask = M.build_bitfield(cfg["segments"])
+    desc = mask.device_descriptors()
+    lay = plan.layout
+    n_tiles = int(plan.assignment.loads[rank].item())
+    ks = {"classify_us": [], "assign_us": [], "plan_build_us": [], "mask_plan_wall_ms": []}
+    for _ in range(reps):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        e[0].record()
+        classes, W = M.classify_device(desc, 128)
+        e[1].record()
+        asg = B.DISTRIBUTIONS[policy](W, world)
+        e[2].record()
+        A.native_plan(desc, classes, W, nq=lay.n_local, n_tiles=n_tiles, owner=asg.owner,
+                      world=world, rank=rank, max_blocks=lay.max_blocks)
+        e[3].record()
+        torch.cuda.synchronize()
+        ks["classify_us"].append(1e3 * e[0].elapsed_time(e[1]))
+        ks["assign_us"].append(1e3 * e[1].elapsed_time(e[2]))
+        ks["plan_build_us"].append(1e3 * e[2].elapsed_time(e[3]))
+        t0 = time.perf_counter()
+        CP.make_cp_plan(M.build_bitfield(cfg["segments"]), world, rank, policy)
+        torch.cuda.synchronize()
+        ks["mask_plan_wall_ms"].append(1e3 * (time.perf_counter() - t0))
+    out = {k: statistics.median(v) for k, v in ks.items()}
+    nb = desc.shape[0] // 128
+    out.update({"blocks": nb, "tiles_classified": nb * nb,
+                "what": "K1+K2 = bam_block_summarize + bam_classify (8*T B read, nb^2 + 4 nb B "
+                        "written), K3 = the policy's assignment kernel(s), plan_build = "
+                        "bam_plan_build; mask_plan_wall_ms = host wall of build_bitfield + "
+                        "make_cp_plan incl. its one sync"})
+    return out
+
+
+def cpu_planning_sample(segments, G, rows=16):
+    """The reference's planning algorithm on the CPU: block_workloads
+    (mask.py:168-188 -- classify every (query block, key block) pair with the
+    OR short-circuit then an exact element count) + lpt_distribute
+    (balance.py:58-76), as restated in oracle/ (pure Python, one core,
+    pinned to the reference's outputs by tests/golden).  Rows are
+    independent, so ``rows`` evenly spaced query-block rows are classified and
+    the time is scaled by nb / rows; LPT runs in full on the resulting W
+    (the oracle's numpy W)."""
+    import numpy as np
+
+    from oracle import balance_ref, mask_ref
+
+    desc, _ = mask_ref.build_bitfield(segments)
+    T = len(desc)
+    ranges = mask_ref.block_ranges(T, 128)
+    nb = len(ranges)
+    pick = sorted({int((i + 0.5) * nb / rows) for i in range(rows)})
+    t0 = time.perf_counter()
+    for b in pick:
+        for kr in ranges:
+            mask_ref.classify_pair(desc, ranges[b], kr)
+    dt = time.perf_counter() - t0
+    W = list(mask_ref.block_workloads_c(np.asarray(desc, np.int64), 128)[1])
+    t1 = time.perf_counter()
+    balance_ref.lpt(W, G)
+    lpt_s = time.perf_counter() - t1
+    return {"block_workloads_s_extrapolated": dt * nb / len(pick), "lpt_distribute_s": lpt_s,
+            "cores": 1, "kind": "port",
+            "sample": f"{len(pick)} of {nb} query-block rows classified (x{nb}/{len(pick)}); "
+                      f"LPT over all {nb} blocks, G={G}",
+            "reference_itself_measured_in_build_container": {
+                "config1_4K_block_workloads_s": 2.37, "config2_32K_block_workloads_s": 172.4,
+                "source": "tests/golden/config{1,2}_workloads.json reference_seconds "
+                          "(make_golden.py ran the reference's block_workloads)"}}
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -227,7 +320,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2503_11367_b200 import _lib, attention as A, cp as CP, mask as M
+    from paper_2503_11367_b200 import _lib, attention as A, balance as B, cp as CP, mask as M
 
     Hq, Hkv = cfg["Hq"], cfg["Hkv"]
     mask = M.build_bitfield(cfg["segments"])
@@ -355,24 +448,49 @@ def main():
                     ev_in[b].record(s_in)
             ev_do[b].record(s_in)
 
-    def e2e_run(n):
+    plan_stream = torch.cuda.Stream(device=dev, priority=-1)   # high priority: planning
+    # kernels interleave with the attention CTAs instead of queueing behind them
+
+    def e2e_run(n, fresh_plan=False):
+        """fresh_plan: every step uses a plan built from a freshly built mask
+        (build_bitfield + make_cp_plan, as a training loop with a new mask per
+        batch), prepared one step ahead on the planning stream while the
+        previous step computes; all of it inside the timed region."""
+        plans, ev_plan = [plan], [None]
+
+        def prepare(s):
+            with torch.cuda.stream(plan_stream):
+                plans.append(CP.make_cp_plan(M.build_bitfield(cfg["segments"]), world, rank,
+                                             args.policy))
+                e = torch.cuda.Event()
+                e.record(plan_stream)
+                ev_plan.append(e)
+
         issue_h2d(0)
+        if fresh_plan:
+            prepare(0)
         for s in range(n):
             b = s % 2
             if s + 1 < n:
                 issue_h2d(s + 1)
             cur.wait_event(ev_in[b])
+            pl = plan
+            if fresh_plan:
+                cur.wait_event(ev_plan[s + 1])
+                pl = plans[s + 1]
             qd, kd, vd = (t.detach().requires_grad_(True) for t in dev_in[b][:3])
             dod = dev_in[b][3]
             if world > 1:
-                o = CP.cp_bitfield_attention(qd, kd, vd, plan, groups=n_groups,
+                o = CP.cp_bitfield_attention(qd, kd, vd, pl, groups=n_groups,
                                              transport=transport)
             else:
-                o = A.bitfield_attention(qd, kd, vd, plan.attn)
+                o = A.bitfield_attention(qd, kd, vd, pl.attn)
             ev_fwd[b].record(cur)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_fwd[b])
                 h_outs[b][0].copy_(o.detach(), non_blocking=True)
+            if fresh_plan and s + 1 < n:
+                prepare(s + 1)            # the next batch's mask + plan, under this step
             cur.wait_event(ev_do[b])
             o.backward(dod)
             outs = (qd.grad, kd.grad, vd.grad)
@@ -384,20 +502,28 @@ def main():
                     src.record_stream(s_out)
                 o.record_stream(s_out)
         cur.wait_stream(s_out)
+        cur.wait_stream(plan_stream)
 
-    e2e_run(1)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    e2e_run(e2e_steps)
-    e1.record()
-    barrier()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    if world > 1:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = tt.item()
+    def e2e_time(fresh_plan):
+        e2e_run(1, fresh_plan)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        e2e_run(e2e_steps, fresh_plan)
+        e1.record()
+        barrier()
+        ms = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = tt.item()
+        return ms
+
+    e2e_ms = e2e_time(False)
+    e2e_fresh_ms = e2e_time(True)
+    planning = time_planning(M, CP, B, A, cfg, world, rank, args.policy, plan)
     e2e_value = flop_step / (e2e_ms * 1e-3) / 1e12
+    e2e_fresh_value = flop_step / (e2e_fresh_ms * 1e-3) / 1e12
 
     peaks, peak_src = load_peaks()
     traffic = None
@@ -425,8 +551,10 @@ def main():
         dt, fl, sample = cpu_attention_sample(cfg["segments"], Hq, Hkv,
                                               sample_blocks(nb, args.cpu_sample_blocks))
         cpu_baseline = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": _t.get_num_threads(),
-                        "kind": "port", "sample": sample + " (fp32 oracle fwd+bwd, torch CPU)",
-                        "seconds": dt}
+                        "kind": "port", "sample": sample + " (fp32 oracle fwd+bwd, torch CPU, "
+                                                           "blockwise-sparse)",
+                        "seconds": dt,
+                        "planning": cpu_planning_sample(cfg["segments"], max(world, cfg["cp"]))}
 
     if rank == 0:
         line = {
@@ -470,7 +598,13 @@ def main():
                     "copies": "pinned host buffers; H2D of step s+1 and D2H of step s on two "
                               "copy streams overlap step s's kernels (double-buffered); "
                               "the forward waits for q/k/v only, the backward for dO, and o "
-                              "is read back during the backward"},
+                              "is read back during the backward",
+                    "fresh_mask_plan_per_step": {
+                        "value": e2e_fresh_value, "ms_per_step": e2e_fresh_ms,
+                        "what": "every step runs on a plan from a freshly built mask "
+                                "(build_bitfield + make_cp_plan), prepared one step ahead on a "
+                                "high-priority planning stream under the previous step"}},
+            "planning": planning,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -49,6 +49,10 @@ typedef struct BamBlockSummary {
 
 const char* bam_last_error(void);
 int bam_version(void);
+/* sizeof of the ABI structs as compiled ("BamAttnFwdParams", "BamAttnBwdParams",
+ * "BamPlan", "BamBlockSummary"), -1 for an unknown name: lets bindings check
+ * their struct layouts against the library. */
+int64_t bam_sizeof(const char* name);
 
 /* ---- bitfield masks (reference src/mmplan/mask.py) ------------------------ */
 
@@ -166,6 +170,11 @@ typedef struct BamAttnFwdParams {
    * kv_ready holds one flag per (rank, KV head): kv_ready[g*Hkv + hkv]. */
   const int32_t* kv_ready;
   int32_t kv_epoch, kv_rank, kv_rows_per_rank, kv_head_major;
+  /* Optional device-side work counts (bam_plan_build's counts[2]): when set, the
+   * host's n_pairs (bam_attn_fwd_qpairs / _2cta) and n_items are upper bounds
+   * that size the grid, and CTAs past dev_counts[0] (pairs) or dev_counts[1]
+   * (items) exit at once -- the plan needs no host synchronisation. */
+  const int32_t* dev_counts;
 } BamAttnFwdParams;
 int bam_attn_fwd(const BamAttnFwdParams* p, void* stream);
 
@@ -263,6 +272,37 @@ int bam_attn_fwd_2cta(const BamAttnFwdParams* p, const int32_t* pair_ids, int32_
 int bam_attn_fwd_qpairs(const BamAttnFwdParams* p, const int32_t* pair_ids, int32_t n_pairs,
                         const int32_t* slot_q, const int32_t* slot_off, const int32_t* slot_tiles,
                         void* stream);
+
+/* ---- per-rank attention planner (no host synchronisation) -------------------
+ * Builds, on `stream`, everything the attention kernels need for one rank of a
+ * CP plan from the tile classes and the block assignment: the rank-major
+ * gathered layout (k_row; this rank's blocks q_gid ascending), the CSR rows
+ * (fwd; `row_tiles` with this rank's key blocks first when world > 1,
+ * `row_tiles_asc` ascending -- the same buffer when world == 1) and CSC
+ * columns (bwd), the heavy-first orders, the backward CTA-pair step lists, the
+ * forward query-block pairs and the whole-row items of the other blocks
+ * (counts[0] shared pairs in fwd_pair_ids, counts[1] items in fwd_rest_items,
+ * both on the device; see BamAttnFwdParams.dev_counts).
+ * Sizes (int32 elements), with n_tiles = sum of W over this rank's blocks (its
+ * LPT load) and P = ceil(nb/2), F = ceil(nq/2): k_row nb, q_gid nq, row_cnt nq,
+ * row_off nq+1, row_tiles / row_tiles_asc / col_tiles n_tiles, col_cnt nb,
+ * col_off nb+1, fwd_order nq, bwd_order nb, slot_kb / slot_cnt 2P, slot_off
+ * 2P+1, slot_tiles 2*n_tiles, pair_shared P, fwd_slot_q / fwd_slot_cnt 2F,
+ * fwd_slot_off 2F+1, fwd_slot_tiles 2*n_tiles, fwd_shared F, fwd_pair_ids F,
+ * fwd_rest_items 4*nq, counts 2.  nb <= 16384 (2M tokens). */
+typedef struct BamPlan {
+  const uint8_t* classes;   /* [nb, nb] from bam_classify */
+  const int32_t* owner;     /* [nb] rank of each block (K3); may be NULL when world == 1 */
+  int32_t nb, nq, world, rank;
+  int32_t max_blocks;       /* the largest per-rank block count (gathered rank stride) */
+  int32_t pad_;
+  int32_t *k_row, *q_gid, *row_cnt, *row_off, *row_tiles, *row_tiles_asc;
+  int32_t *col_cnt, *col_off, *col_tiles, *fwd_order, *bwd_order;
+  int32_t *slot_kb, *slot_cnt, *slot_off, *slot_tiles, *pair_shared;
+  int32_t *fwd_slot_q, *fwd_slot_cnt, *fwd_slot_off, *fwd_slot_tiles, *fwd_shared;
+  int32_t *fwd_pair_ids, *fwd_rest_items, *counts;
+} BamPlan;
+int bam_plan_build(const BamPlan* plan, void* stream);
 
 /* Stream-ordered 32-bit store (cuStreamWriteValue32, executed without an SM
  * after the stream's prior work, with a memory barrier): the arrival flags of

@@ -28,12 +28,17 @@ import torch
 from .mask_ref import dense_rows
 
 
-def _rows_mask(desc_np: np.ndarray, rows: np.ndarray) -> torch.Tensor:
-    return torch.from_numpy(dense_rows(desc_np, rows))
+def _rows_mask(desc_np: np.ndarray, rows: np.ndarray, cols=None) -> torch.Tensor:
+    return torch.from_numpy(dense_rows(desc_np, rows, cols))
 
 
-def attention_fwd(q, k, v, desc, q_pos, scale=None, chunk=512):
-    """Returns (O fp32 [Tq, Hq, d], LSE fp32 [Hq, Tq])."""
+def attention_fwd(q, k, v, desc, q_pos, scale=None, chunk=512, k_pos=None):
+    """Returns (O fp32 [Tq, Hq, d], LSE fp32 [Hq, Tq]).
+
+    ``k_pos``: global positions of the rows of k/v (default: 0..Tk-1, the
+    whole sequence).  Passing only the keys of a query block's non-skip
+    tiles computes the same rows blockwise-sparse: skipped
+    tiles contribute nothing."""
     q, k, v = q.float(), k.float(), v.float()
     Tq, Hq, d = q.shape
     Hkv = k.shape[1]
@@ -45,9 +50,10 @@ def attention_fwd(q, k, v, desc, q_pos, scale=None, chunk=512):
     LSE = torch.empty(Hq, Tq)
     kk = k.permute(1, 0, 2)     # [Hkv, Tk, d]
     vv = v.permute(1, 0, 2)
+    kp = None if k_pos is None else np.asarray(k_pos, dtype=np.int64)
     for r0 in range(0, Tq, chunk):
         r1 = min(r0 + chunk, Tq)
-        allow = _rows_mask(desc_np, pos[r0:r1])                    # [R, Tk]
+        allow = _rows_mask(desc_np, pos[r0:r1], kp)                # [R, Tk]
         qh = q[r0:r1].permute(1, 0, 2).reshape(Hkv, grp * (r1 - r0), d)
         s = torch.bmm(qh, kk.transpose(1, 2)).view(Hkv, grp, r1 - r0, -1) * scale
         s = s.masked_fill(~allow, float("-inf"))
@@ -59,10 +65,10 @@ def attention_fwd(q, k, v, desc, q_pos, scale=None, chunk=512):
     return O, LSE
 
 
-def attention_bwd(q, k, v, o, lse, do, desc, q_pos, scale=None, chunk=512):
+def attention_bwd(q, k, v, o, lse, do, desc, q_pos, scale=None, chunk=512, k_pos=None):
     """Gradients of sum(O * dO).  Returns (dQ [Tq, Hq, d], dK, dV [Tk, Hkv, d]),
     fp32; dK/dV are the contributions of these query rows only (the CP
-    partials that a reduce-scatter sums)."""
+    partials that a reduce-scatter sums).  ``k_pos`` as in attention_fwd."""
     q, k, v, o, do = q.float(), k.float(), v.float(), o.float(), do.float()
     Tq, Hq, d = q.shape
     Tk, Hkv, _ = k.shape
@@ -76,10 +82,11 @@ def attention_bwd(q, k, v, o, lse, do, desc, q_pos, scale=None, chunk=512):
     kk = k.permute(1, 0, 2)
     vv = v.permute(1, 0, 2)
     D_all = (do * o).sum(-1)                                        # [Tq, Hq]
+    kp = None if k_pos is None else np.asarray(k_pos, dtype=np.int64)
     for r0 in range(0, Tq, chunk):
         r1 = min(r0 + chunk, Tq)
         R = r1 - r0
-        allow = _rows_mask(desc_np, pos[r0:r1])
+        allow = _rows_mask(desc_np, pos[r0:r1], kp)
         qh = q[r0:r1].permute(1, 0, 2).reshape(Hkv, grp * R, d)
         doh = do[r0:r1].permute(1, 0, 2).reshape(Hkv, grp * R, d)
         s = torch.bmm(qh, kk.transpose(1, 2)).view(Hkv, grp, R, Tk) * scale

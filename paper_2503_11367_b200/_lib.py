@@ -32,7 +32,20 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("items", c_vp), ("part_o", c_vp), ("part_ml", c_vp), ("n_items", c_i32),
                 ("pad_", c_i32), ("kv_ready", c_vp), ("kv_epoch", c_i32), ("kv_rank", c_i32),
-                ("kv_rows_per_rank", c_i32), ("kv_head_major", c_i32)]
+                ("kv_rows_per_rank", c_i32), ("kv_head_major", c_i32), ("dev_counts", c_vp)]
+
+
+PLAN_BUFFERS = ("k_row", "q_gid", "row_cnt", "row_off", "row_tiles", "row_tiles_asc", "col_cnt",
+                "col_off", "col_tiles", "fwd_order", "bwd_order", "slot_kb", "slot_cnt",
+                "slot_off", "slot_tiles", "pair_shared", "fwd_slot_q", "fwd_slot_cnt",
+                "fwd_slot_off", "fwd_slot_tiles", "fwd_shared", "fwd_pair_ids",
+                "fwd_rest_items", "counts")
+
+
+class BamPlan(ctypes.Structure):
+    _fields_ = ([("classes", c_vp), ("owner", c_vp), ("nb", c_i32), ("nq", c_i32),
+                 ("world", c_i32), ("rank", c_i32), ("max_blocks", c_i32), ("pad_", c_i32)] +
+                [(n, c_vp) for n in PLAN_BUFFERS])
 
 
 class BamAttnBwdParams(ctypes.Structure):
@@ -51,6 +64,7 @@ class BamAttnBwdParams(ctypes.Structure):
 SIGNATURES = {
     "bam_last_error": (ctypes.c_char_p, []),
     "bam_version": (c_i32, []),
+    "bam_sizeof": (c_i64, [ctypes.c_char_p]),
     "bam_mask_expand": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
     "bam_mask_validate": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
     "bam_block_summarize": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_vp]),
@@ -83,6 +97,7 @@ SIGNATURES = {
                                     c_vp, c_vp]),
     "bam_build_pair_lists": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bam_selftest_umma": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bam_plan_build": (c_i32, [ctypes.POINTER(BamPlan), c_vp]),
     "bam_set_trace_buffer": (c_i32, [c_vp]),
 }
 
@@ -144,7 +159,7 @@ KERNELS_PER_CALL = {
     "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
     "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
     "bam_reduce_partials_bf16": 1,
-    "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1,
+    "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1, "bam_plan_build": 15,
     "bam_stream_write_i32": 0, "bam_stream_wait_i32_geq": 0,   # stream memory operations
 }
 launch_count = 0

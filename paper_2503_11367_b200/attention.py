@@ -33,6 +33,10 @@ HEAD_DIM = 128
 
 @dataclass
 class AttentionPlan:
+    """Everything the kernels need for one rank (``bam_plan_build``); int32
+    device views into one workspace.  Forward pair / item lists are sized by
+    their upper bounds; ``counts`` (device) holds the real lengths, which the
+    kernels read (``BamAttnFwdParams.dev_counts``)."""
     desc: torch.Tensor        # int64 [nb*128]
     nb: int
     classes: torch.Tensor     # uint8 [nb, nb]
@@ -41,7 +45,7 @@ class AttentionPlan:
     k_row: torch.Tensor       # int32 [nb] block-row of global block kb in k/v
     k_rows: int
     row_off: torch.Tensor     # int32 [nq+1]
-    row_tiles: torch.Tensor   # int32 kb << 2 | class
+    row_tiles: torch.Tensor   # int32 kb << 2 | class (this rank's key blocks first under CP)
     col_off: torch.Tensor     # int32 [nb+1]
     col_tiles: torch.Tensor   # int32 j << 2 | class
     fwd_order: torch.Tensor   # int32 [nq] heavy-first local query blocks
@@ -51,103 +55,82 @@ class AttentionPlan:
     slot_off: torch.Tensor | None = None
     slot_tiles: torch.Tensor | None = None
     pair_shared: torch.Tensor | None = None
-    # forward CTA pairs (cta_group::2): shared pairs of heavy-first query blocks
-    # and a whole-row items list (j, 0, W, -1) for the blocks of the other pairs
+    # forward query-block pairs: shared pairs (fwd_pair_ids, counts[0] of them) and
+    # whole-row items (j, 0, W, -1) for the blocks of the other pairs (counts[1])
     fwd_pair_ids: torch.Tensor | None = None
     fwd_slot_q: torch.Tensor | None = None
     fwd_slot_off: torch.Tensor | None = None
     fwd_slot_tiles: torch.Tensor | None = None
     fwd_rest_items: torch.Tensor | None = None
+    counts: torch.Tensor | None = None
+    row_cnt: torch.Tensor | None = None
+    col_cnt: torch.Tensor | None = None
 
     @property
     def nq(self) -> int:
         return int(self.q_gid.shape[0])
 
 
-def _heavy_first(counts: torch.Tensor) -> torch.Tensor:
-    # stable sort by descending tile count (ties: lower index first)
-    return torch.sort(-counts.to(torch.int64), stable=True).indices.to(torch.int32)
+def _plan_sizes(nb: int, nq: int, n_tiles: int) -> dict:
+    """int32 element counts of bam_plan_build's buffers (include/bam.h)."""
+    P, F, t = (nb + 1) // 2, (nq + 1) // 2, max(n_tiles, 1)
+    return {"k_row": nb, "q_gid": nq, "row_cnt": nq, "row_off": nq + 1, "row_tiles": t,
+            "row_tiles_asc": t, "col_cnt": nb, "col_off": nb + 1, "col_tiles": t,
+            "fwd_order": nq, "bwd_order": nb, "slot_kb": 2 * P, "slot_cnt": 2 * P,
+            "slot_off": 2 * P + 1, "slot_tiles": 2 * t, "pair_shared": P, "fwd_slot_q": 2 * F,
+            "fwd_slot_cnt": 2 * F, "fwd_slot_off": 2 * F + 1, "fwd_slot_tiles": 2 * t,
+            "fwd_shared": F, "fwd_pair_ids": F, "fwd_rest_items": 4 * nq, "counts": 2}
 
 
-def build_plan(desc: torch.Tensor, q_gid: torch.Tensor | None = None,
-               k_row: torch.Tensor | None = None, k_rows: int | None = None,
-               classes: torch.Tensor | None = None, W: torch.Tensor | None = None) -> AttentionPlan:
-    """Plan for query blocks ``q_gid`` (default: all, in order) against all
-    keys at block-rows ``k_row`` (default identity)."""
+def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, nq: int,
+                n_tiles: int, owner: torch.Tensor | None = None, world: int = 1,
+                rank: int = 0, max_blocks: int | None = None) -> AttentionPlan:
+    """One ``bam_plan_build`` call on the current stream (no host sync): the
+    gathered layout (k_row, this rank's q_gid), tile lists, heavy-first
+    orders, backward CTA pairs and forward query-block pairs.  ``nq``,
+    ``max_blocks`` and ``n_tiles`` (sum of W over the rank's blocks) size the
+    buffers; under CP they come from the assignment's one D2H."""
+    nb = classes.shape[0]
+    max_blocks = nq if max_blocks is None else max_blocks
+    sizes = _plan_sizes(nb, nq, n_tiles)
+    if world == 1:
+        sizes.pop("row_tiles_asc")            # one buffer: the rows are ascending either way
+    ws = torch.empty(sum(sizes.values()), dtype=torch.int32, device=classes.device)
+    views, off = {}, 0
+    for name, n in sizes.items():
+        views[name] = ws[off:off + n]
+        off += n
+    if world == 1:
+        views["row_tiles_asc"] = views["row_tiles"]
+    bp = _lib.BamPlan(classes.data_ptr(), owner.data_ptr() if owner is not None else None, nb,
+                      nq, world, rank, max_blocks, 0,
+                      *[views[name].data_ptr() for name in _lib.PLAN_BUFFERS])
+    _lib.call("bam_plan_build", bp)
+    return AttentionPlan(
+        desc=desc, nb=nb, classes=classes, W=W, q_gid=views["q_gid"], k_row=views["k_row"],
+        k_rows=world * max_blocks, row_off=views["row_off"], row_tiles=views["row_tiles"],
+        col_off=views["col_off"], col_tiles=views["col_tiles"], fwd_order=views["fwd_order"],
+        bwd_order=views["bwd_order"], slot_kb=views["slot_kb"], slot_off=views["slot_off"],
+        slot_tiles=views["slot_tiles"], pair_shared=views["pair_shared"],
+        fwd_pair_ids=views["fwd_pair_ids"], fwd_slot_q=views["fwd_slot_q"],
+        fwd_slot_off=views["fwd_slot_off"], fwd_slot_tiles=views["fwd_slot_tiles"],
+        fwd_rest_items=views["fwd_rest_items"].view(nq, 4), counts=views["counts"],
+        row_cnt=views["row_cnt"], col_cnt=views["col_cnt"])
+
+
+def build_plan(desc: torch.Tensor, classes: torch.Tensor | None = None,
+               W: torch.Tensor | None = None) -> AttentionPlan:
+    """Single-GPU plan: every query block against every key block (identity
+    layout).  One host sync (the tile count that sizes the lists)."""
     _lib.require_cuda()
     T = desc.shape[0]
     if T % BLOCK:
         raise ValueError(f"attention needs T % {BLOCK} == 0 (T={T})")
     nb = T // BLOCK
-    dev = desc.device
     if classes is None:
         classes, W = classify_device(desc, BLOCK)
-    if q_gid is None:
-        q_gid = torch.arange(nb, dtype=torch.int32, device=dev)
-    if k_row is None:
-        k_row = torch.arange(nb, dtype=torch.int32, device=dev)
-        k_rows = nb
-    nq = int(q_gid.shape[0])
-    row_cnt = torch.empty(nq, dtype=torch.int32, device=dev)
-    row_off = torch.empty(nq + 1, dtype=torch.int32, device=dev)
-    col_cnt = torch.empty(nb, dtype=torch.int32, device=dev)
-    col_off = torch.empty(nb + 1, dtype=torch.int32, device=dev)
-    _lib.call("bam_build_tile_lists", classes.data_ptr(), nb, q_gid.data_ptr(), nq,
-              row_cnt.data_ptr(), row_off.data_ptr(), None, col_cnt.data_ptr(), col_off.data_ptr(),
-              None)
-    n_row = int(row_off[-1].item())
-    n_col = int(col_off[-1].item())
-    row_tiles = torch.empty(max(n_row, 1), dtype=torch.int32, device=dev)
-    col_tiles = torch.empty(max(n_col, 1), dtype=torch.int32, device=dev)
-    _lib.call("bam_build_tile_lists", classes.data_ptr(), nb, q_gid.data_ptr(), nq,
-              row_cnt.data_ptr(), row_off.data_ptr(), row_tiles.data_ptr(), col_cnt.data_ptr(),
-              col_off.data_ptr(), col_tiles.data_ptr())
-    bwd_order = _heavy_first(col_cnt)
-    npairs = (nb + 1) // 2
-    slot_kb = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
-    slot_cnt = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
-    slot_off = torch.empty(2 * npairs + 1, dtype=torch.int32, device=dev)
-    pair_shared = torch.empty(npairs, dtype=torch.int32, device=dev)
-    _lib.call("bam_build_pair_lists", col_off.data_ptr(), col_tiles.data_ptr(),
-              bwd_order.data_ptr(), nb, slot_kb.data_ptr(), slot_cnt.data_ptr(),
-              slot_off.data_ptr(), None, pair_shared.data_ptr())
-    slot_tiles = torch.empty(max(int(slot_off[-1].item()), 1), dtype=torch.int32, device=dev)
-    _lib.call("bam_build_pair_lists", col_off.data_ptr(), col_tiles.data_ptr(),
-              bwd_order.data_ptr(), nb, slot_kb.data_ptr(), slot_cnt.data_ptr(),
-              slot_off.data_ptr(), slot_tiles.data_ptr(), pair_shared.data_ptr())
-    fwd_order = _heavy_first(row_cnt)
-    fp = _fwd_pairs(row_off, row_tiles, row_cnt, fwd_order, nq, dev)
-    return AttentionPlan(desc=desc, nb=nb, classes=classes, W=W, q_gid=q_gid.to(torch.int32),
-                         k_row=k_row.to(torch.int32), k_rows=int(k_rows), row_off=row_off,
-                         row_tiles=row_tiles, col_off=col_off, col_tiles=col_tiles,
-                         fwd_order=fwd_order, bwd_order=bwd_order, slot_kb=slot_kb,
-                         slot_off=slot_off, slot_tiles=slot_tiles, pair_shared=pair_shared, **fp)
-
-
-def _fwd_pairs(row_off, row_tiles, row_cnt, fwd_order, nq, dev) -> dict:
-    """Pairs of consecutive heavy-first query blocks (bam_build_pair_lists over
-    the row lists): shared pairs run on CTA pairs (bam_attn_fwd_2cta), the
-    blocks of the other pairs as whole-row work items of the one-CTA kernel."""
-    npairs = (nq + 1) // 2
-    slot_q = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
-    slot_cnt = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
-    slot_off = torch.empty(2 * npairs + 1, dtype=torch.int32, device=dev)
-    shared = torch.empty(npairs, dtype=torch.int32, device=dev)
-    _lib.call("bam_build_pair_lists", row_off.data_ptr(), row_tiles.data_ptr(),
-              fwd_order.data_ptr(), nq, slot_q.data_ptr(), slot_cnt.data_ptr(),
-              slot_off.data_ptr(), None, shared.data_ptr())
-    slot_tiles = torch.empty(max(int(slot_off[-1].item()), 1), dtype=torch.int32, device=dev)
-    _lib.call("bam_build_pair_lists", row_off.data_ptr(), row_tiles.data_ptr(),
-              fwd_order.data_ptr(), nq, slot_q.data_ptr(), slot_cnt.data_ptr(),
-              slot_off.data_ptr(), slot_tiles.data_ptr(), shared.data_ptr())
-    sh = shared.bool()
-    pair_ids = torch.nonzero(sh).flatten().to(torch.int32)
-    rest = slot_q.view(npairs, 2)[~sh].flatten()
-    rest = rest[rest >= 0].to(torch.int64)
-    items = torch.stack([rest, torch.zeros_like(rest), row_cnt.to(torch.int64)[rest],
-                         torch.full_like(rest, -1)], dim=1).to(torch.int32).contiguous()
-    return dict(fwd_pair_ids=pair_ids, fwd_slot_q=slot_q, fwd_slot_off=slot_off,
-                fwd_slot_tiles=slot_tiles, fwd_rest_items=items)
+    n_tiles = int(W.sum().item())
+    return native_plan(desc, classes, W, nq=nb, n_tiles=n_tiles)
 
 
 def plan_for_mask(mask: BitfieldMask) -> AttentionPlan:
@@ -287,6 +270,8 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         part_ml.data_ptr() if part_ml is not None else None,
         schedule.n_items if schedule is not None else 0, 0)
     p.kv_head_major = int(kv_head_major)
+    if plan.counts is not None and schedule is None:
+        p.dev_counts = plan.counts.data_ptr()
     if kv_ready is not None:
         # the head-pair, query-pair and one-head kernels honour the flags (not the
         # CTA-pair kernel, nor split-KV schedules)

@@ -54,7 +54,10 @@ class CPLayout:
 
 
 def cp_layout(owner: torch.Tensor, world: int, rank: int) -> CPLayout:
-    """Index plumbing from an owner vector (device or CPU tensor)."""
+    """Index plumbing from an owner vector (device or CPU tensor), with torch
+    ops: the host-side statement of the layout that ``make_cp_plan`` builds
+    on the device (``bam_plan_build``'s layout kernel; tests compare them).
+    Used by the CPU (gloo) exchange tests and tools."""
     owner = owner.to(torch.int64)
     nb = owner.shape[0]
     order = torch.sort(owner, stable=True).indices          # blocks grouped by rank, ascending id
@@ -390,36 +393,31 @@ class CPPlan:
 def make_cp_plan(mask_or_desc, world: int, rank: int, policy: str = "lpt") -> CPPlan:
     """Classify the mask (replicated, deterministic on every rank), assign
     query blocks with ``policy`` ("lpt" | "zigzag" | "contiguous") and build
-    this rank's attention plan.  Every rank computes the identical plan, so
-    no plan exchange is needed."""
+    this rank's attention plan (``bam_plan_build``).  Every rank computes the
+    identical plan, so no plan exchange is needed.
+
+    All on the current stream with ONE host synchronisation: the D2H of the
+    assignment's per-rank offsets and loads, which give the shapes (this
+    rank's block count, the padded rank stride, the tile-list length).  Run it
+    on a side stream to build the next batch's plan under this batch's
+    attention."""
     desc = (mask_or_desc.device_descriptors() if isinstance(mask_or_desc, BitfieldMask)
             else mask_or_desc)
     if desc.shape[0] % BLOCK:
         raise ValueError(f"CP attention needs T % {BLOCK} == 0")
     classes, W = classify_device(desc, BLOCK)
     asg = B.DISTRIBUTIONS[policy](W, world)
-    layout = cp_layout(asg.owner, world, rank)
-    attn = A.build_plan(desc, q_gid=layout.local_blocks, k_row=layout.k_row,
-                        k_rows=world * layout.max_blocks, classes=classes, W=W)
-    _local_tiles_first(attn, layout)
+    host = torch.cat([asg.off.to(torch.int64), asg.loads]).cpu().tolist()   # the one sync
+    off, loads = host[:world + 1], host[world + 1:]
+    counts = [off[g + 1] - off[g] for g in range(world)]
+    if counts[rank] == 0:
+        raise ValueError(f"rank {rank} owns no query block ({len(W)} blocks over {world} ranks)")
+    max_blocks = max(counts)
+    attn = A.native_plan(desc, classes, W, nq=counts[rank], n_tiles=loads[rank],
+                         owner=asg.owner, world=world, rank=rank, max_blocks=max_blocks)
+    layout = CPLayout(world=world, rank=rank, owner=asg.owner, local_blocks=attn.q_gid,
+                      k_row=attn.k_row, counts=counts, max_blocks=max_blocks)
     return CPPlan(layout=layout, attn=attn, assignment=asg, policy=policy)
-
-
-def _local_tiles_first(attn: A.AttentionPlan, layout: CPLayout) -> None:
-    """Reorder every query row's key tiles so that the tiles of keys this rank
-    owns come first (stable otherwise): with the copy-engine exchange the
-    forward works on them while the peers' K/V are still being pulled.  The
-    online softmax does not depend on the tile order; the backward's column
-    lists and the query-pair union lists are separate arrays."""
-    n = int(attn.row_off[-1].item())
-    if n == 0 or layout.world == 1:
-        return
-    rt = attn.row_tiles[:n]
-    remote = (layout.owner.to(torch.int64)[(rt >> 2).to(torch.int64)] != layout.rank)
-    counts = (attn.row_off[1:] - attn.row_off[:-1]).to(torch.int64)
-    row = torch.repeat_interleave(torch.arange(counts.shape[0], device=rt.device), counts)
-    order = torch.sort(row * 2 + remote.to(torch.int64), stable=True).indices
-    attn.row_tiles[:n] = rt[order]
 
 
 _COMM_STREAMS: dict = {}
@@ -452,7 +450,7 @@ def resolve_transport(transport: str, plan: "CPPlan", hkv: int, d: int, device,
     never run different transports; it is decided once per group.  "auto"
     at world 1 needs no exchange ("local"); a forced "nccl" / "ce" runs the
     exchange even then (a one-rank process group)."""
-    if transport not in TRANSPORTS:
+    if transport not in TRANSPORTS and transport != "local":
         raise ValueError(f"transport must be one of {TRANSPORTS}")
     if transport != "auto":
         return transport

@@ -11,11 +11,10 @@
 // min-reduction per item.  The sort key is (INT32_MAX - w) << 32 | id.
 #include "../../include/bam.h"
 #include "common.cuh"
+#include "kernels.cuh"
 #include "scan.cuh"
 
 namespace bam {
-
-constexpr int kSortSmemMax = 16384;  // items sorted in one CTA's shared memory
 
 __device__ __forceinline__ uint64_t lpt_key(int32_t w, int64_t i) {
   return (uint64_t(uint32_t(0x7FFFFFFF - w)) << 32) | uint64_t(uint32_t(i));
@@ -24,7 +23,8 @@ __device__ __forceinline__ uint64_t lpt_key(int32_t w, int64_t i) {
 // One-CTA bitonic sort in shared memory (n_pad power of two <= kSortSmemMax).
 __global__ void __launch_bounds__(1024) sort_smem_kernel(const int32_t* __restrict__ w,
                                                          int64_t n, int64_t n_pad,
-                                                         uint64_t* __restrict__ sorted) {
+                                                         uint64_t* __restrict__ sorted,
+                                                         int32_t* __restrict__ order) {
   extern __shared__ uint64_t keys[];
   for (int64_t i = threadIdx.x; i < n_pad; i += blockDim.x)
     keys[i] = i < n ? lpt_key(w[i], i) : ~0ull;
@@ -45,7 +45,10 @@ __global__ void __launch_bounds__(1024) sort_smem_kernel(const int32_t* __restri
       __syncthreads();
     }
   }
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sorted[i] = keys[i];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    if (sorted) sorted[i] = keys[i];
+    if (order) order[i] = (int32_t)uint32_t(keys[i]);
+  }
 }
 
 // Multi-CTA bitonic sort in global memory for large n: init + one launch per stage.
@@ -260,7 +263,7 @@ int bam_lpt_assign(const int32_t* w, int64_t n, int32_t G, int32_t* owner, int32
     const size_t smem = np * sizeof(uint64_t);
     BAM_CUDA_TRY(cudaFuncSetAttribute(sort_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-    sort_smem_kernel<<<1, 1024, smem, s>>>(w, n, np, keys);
+    sort_smem_kernel<<<1, 1024, smem, s>>>(w, n, np, keys, nullptr);
     BAM_LAUNCH_CHECK();
   } else {
     const int grid = 148 * 8;

@@ -37,6 +37,7 @@
 // aids BAM_TRACE, BAM_EXPERIMENT_MMA_ONLY, BAM_EXPERIMENT_NO_DQ_RED.
 #include "../../include/bam.h"
 #include "common.cuh"
+#include "kernels.cuh"
 #include "scan.cuh"
 #include "tma.h"
 

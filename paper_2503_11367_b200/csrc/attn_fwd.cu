@@ -264,6 +264,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
   const int h = p.h_begin + (kRowMajor ? blockIdx.y : blockIdx.x);
+  // device-counted items (bam_plan_build): the grid is an upper bound
+  if (p.dev_counts && p.items && (int)(kRowMajor ? blockIdx.x : blockIdx.y) >= p.dev_counts[1])
+    return;
   const WorkItem wi = work_item(p, kRowMajor ? blockIdx.x : blockIdx.y);
   const int j = wi.j, n = wi.n, slot = wi.slot;
   const int32_t* tiles = wi.tiles;
@@ -594,6 +597,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
   const int bx = kRowMajor ? blockIdx.x : blockIdx.y, by = kRowMajor ? blockIdx.y : blockIdx.x;
   int jj[2], hh[2], n, slot;
   const int32_t* tl[2];
+  // device-counted pairs / items (bam_plan_build): the grid is an upper bound
+  if (p.dev_counts && (kQPair || p.items) && bx >= p.dev_counts[kQPair ? 0 : 1]) return;
   if constexpr (kQPair) {
     const int pr = pair_ids[bx];
     for (int i = 0; i < 2; ++i) {
@@ -784,6 +789,7 @@ __global__ void __maxnreg__(168)
   const uint32_t crank = cluster_ctarank();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
   const int h0 = p.h_begin + 2 * blockIdx.y;
+  if (p.dev_counts && (int)(blockIdx.x >> 1) >= p.dev_counts[0]) return;  // both CTAs of the pair
   const int slot = 2 * pair_ids[blockIdx.x >> 1] + (int)crank;
   const int j = slot_q[slot];
   const int32_t* tiles = slot_tiles + slot_off[slot];

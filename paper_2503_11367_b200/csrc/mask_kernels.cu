@@ -17,6 +17,7 @@
 
 #include "../../include/bam.h"
 #include "common.cuh"
+#include "kernels.cuh"
 #include "scan.cuh"
 
 namespace bam {
@@ -209,11 +210,15 @@ __global__ void list_count_kernel(const uint8_t* __restrict__ classes, int64_t n
   if (threadIdx.x == 0) row_cnt[j] = s;
 }
 
-// Ordered compaction of one row (fwd) by one CTA using ballots.
+// Ordered compaction of one row (fwd) by one CTA using ballots.  With
+// ``owner`` (context parallelism) the row's key blocks owned by ``rank`` come
+// first, then the others, each group in increasing kb: the forward works on
+// local K/V while the peers' rows are still arriving.
 __global__ void list_fill_rows_kernel(const uint8_t* __restrict__ classes, int64_t nb,
                                       const int32_t* __restrict__ q_gid,
                                       const int32_t* __restrict__ row_off,
-                                      int32_t* __restrict__ row_tiles) {
+                                      int32_t* __restrict__ row_tiles,
+                                      const int32_t* __restrict__ owner, int32_t rank) {
   __shared__ int warp_tot[32];
   __shared__ int carry;
   const int j = blockIdx.x;
@@ -221,22 +226,25 @@ __global__ void list_fill_rows_kernel(const uint8_t* __restrict__ classes, int64
   int32_t* out = row_tiles + row_off[j];
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int64_t base = 0; base < nb; base += blockDim.x) {
-    const int64_t kb = base + threadIdx.x;
-    const int cls = kb < nb ? r[kb] : 0;
-    const uint32_t m = __ballot_sync(0xffffffffu, cls != 0);
-    if (lane_id() == 0) warp_tot[threadIdx.x >> 5] = __popc(m);
-    __syncthreads();
-    int before = carry;
-    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) before += warp_tot[w];
-    if (cls) out[before + __popc(m & ((1u << lane_id()) - 1))] = (int32_t)((kb << 2) | cls);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += warp_tot[w];
-      carry += t;
+  for (int pass = 0; pass < (owner ? 2 : 1); ++pass) {
+    for (int64_t base = 0; base < nb; base += blockDim.x) {
+      const int64_t kb = base + threadIdx.x;
+      int cls = kb < nb ? r[kb] : 0;
+      if (owner && cls && ((owner[kb] == rank) != (pass == 0))) cls = 0;
+      const uint32_t m = __ballot_sync(0xffffffffu, cls != 0);
+      if (lane_id() == 0) warp_tot[threadIdx.x >> 5] = __popc(m);
+      __syncthreads();
+      int before = carry;
+      for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) before += warp_tot[w];
+      if (cls) out[before + __popc(m & ((1u << lane_id()) - 1))] = (int32_t)((kb << 2) | cls);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += warp_tot[w];
+        carry += t;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -375,7 +383,7 @@ int bam_build_tile_lists(const uint8_t* classes, int64_t nb, const int32_t* q_gi
   scan_kernel<<<1, 1024, 0, s>>>(col_cnt, nb, col_off);
   BAM_LAUNCH_CHECK();
   if (row_tiles) {
-    list_fill_rows_kernel<<<nq, 256, 0, s>>>(classes, nb, q_gid, row_off, row_tiles);
+    list_fill_rows_kernel<<<nq, 256, 0, s>>>(classes, nb, q_gid, row_off, row_tiles, nullptr, 0);
     BAM_LAUNCH_CHECK();
   }
   if (col_tiles) {

@@ -1,0 +1,200 @@
+// Per-rank attention planner: everything between the block assignment (K3,
+// ref balance.py:58-102) and the attention kernels, on one stream with no
+// host synchronisation (bam_plan_build, include/bam.h).
+//
+//   layout_kernel        owner[nb] -> k_row[nb] (rank-major gathered block-row),
+//                        q_gid[nq] (this rank's blocks, ascending)
+//   list_* kernels       CSR rows (fwd) / CSC columns (bwd) of non-skip tiles
+//   sort_smem_kernel     heavy-first processing orders (-count, index)
+//   pair_lists_kernel    CTA-pair step lists (bwd) / query-block pairs (fwd)
+//   fwd_pairs_kernel     compaction of the shared forward pairs and the
+//                        whole-row items of the others, with device counts
+//                        that the forward kernels read (grid = upper bound)
+//
+// The caller sizes every buffer from (nb, nq, n_tiles): n_tiles = sum of W
+// over this rank's blocks = the rank's LPT load, known on the host after the
+// one D2H of the assignment's (off, loads) that also gives nq and max_blocks.
+#include "../../include/bam.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "scan.cuh"
+
+namespace bam {
+
+// One CTA per rank g: ordered (ascending block id) compaction of the blocks
+// with owner == g.  k_row[b] = g * max_blocks + position; rank's own blocks
+// also go to q_gid.
+__global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict__ owner,
+                                                      int32_t nb, int32_t max_blocks,
+                                                      int32_t rank, int32_t* __restrict__ k_row,
+                                                      int32_t* __restrict__ q_gid) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  const int g = blockIdx.x;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += blockDim.x) {
+    const int b = base + threadIdx.x;
+    const bool mine = b < nb && (owner ? owner[b] : 0) == g;
+    const uint32_t m = __ballot_sync(0xffffffffu, mine);
+    if (lane_id() == 0) warp_tot[threadIdx.x >> 5] = __popc(m);
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) before += warp_tot[w];
+    if (mine) {
+      const int pos = before + __popc(m & ((1u << lane_id()) - 1));
+      k_row[b] = g * max_blocks + pos;
+      if (g == rank) q_gid[pos] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += warp_tot[w];
+      carry += t;
+    }
+    __syncthreads();
+  }
+}
+
+// Forward query-block pairs: the shared pairs (ascending pair id) run in the
+// split-row kernel, the blocks of the other pairs (pair order, then slot) as
+// whole-row items {j, 0, W_j, -1} of the one-head kernel.  counts = {#pairs,
+// #items}.  One CTA, ordered ballot compaction of both lists.
+__global__ void __launch_bounds__(1024) fwd_pairs_kernel(const int32_t* __restrict__ shared,
+                                                         const int32_t* __restrict__ slot_q,
+                                                         const int32_t* __restrict__ row_cnt,
+                                                         int32_t npairs,
+                                                         int32_t* __restrict__ pair_ids,
+                                                         int4* __restrict__ items,
+                                                         int32_t* __restrict__ counts) {
+  __shared__ int wp[32], wi[32];
+  __shared__ int cp, ci;
+  if (threadIdx.x == 0) cp = ci = 0;
+  __syncthreads();
+  for (int base = 0; base < npairs; base += blockDim.x) {
+    const int pr = base + threadIdx.x;
+    const bool valid = pr < npairs;
+    const bool sh = valid && shared[pr] != 0;
+    const int a = valid ? slot_q[2 * pr] : -1, b = valid ? slot_q[2 * pr + 1] : -1;
+    const int n_it = (valid && !sh) ? (a >= 0) + (b >= 0) : 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, sh);
+    // per-warp inclusive scan of the item counts
+    int x = n_it;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane_id() >= (uint32_t)o) x += y;
+    }
+    if (lane_id() == 31) {
+      wp[threadIdx.x >> 5] = __popc(m);
+      wi[threadIdx.x >> 5] = x;
+    }
+    __syncthreads();
+    int bp = cp, bi = ci;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) {
+      bp += wp[w];
+      bi += wi[w];
+    }
+    if (sh) pair_ids[bp + __popc(m & ((1u << lane_id()) - 1))] = pr;
+    int pos = bi + x - n_it;
+    if (n_it) {
+      if (a >= 0) items[pos++] = make_int4(a, 0, row_cnt[a], -1);
+      if (b >= 0) items[pos++] = make_int4(b, 0, row_cnt[b], -1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        cp += wp[w];
+        ci += wi[w];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = cp;
+    counts[1] = ci;
+  }
+}
+
+static int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+static int heavy_first(const int32_t* cnt, int32_t n, int32_t* order, cudaStream_t s) {
+  const int64_t np = next_pow2(n);
+  BAM_CHECK_ARG(np <= kSortSmemMax, "bam_plan_build: %d blocks exceed the one-CTA sort (%d)", n,
+                kSortSmemMax);
+  const size_t smem = np * sizeof(uint64_t);
+  BAM_CUDA_TRY(cudaFuncSetAttribute(sort_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  sort_smem_kernel<<<1, 1024, smem, s>>>(cnt, n, np, nullptr, order);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+}  // namespace bam
+
+using namespace bam;
+
+extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
+  BAM_CHECK_ARG(pp != nullptr, "bam_plan_build: null plan");
+  const BamPlan& p = *pp;
+  BAM_CHECK_ARG(p.classes && p.nb >= 1 && p.nq >= 1 && p.world >= 1 && p.rank >= 0 &&
+                    p.rank < p.world && p.max_blocks >= p.nq,
+                "bam_plan_build: nb=%d nq=%d world=%d rank=%d max_blocks=%d", p.nb, p.nq, p.world,
+                p.rank, p.max_blocks);
+  BAM_CHECK_ARG(p.world == 1 || p.owner, "bam_plan_build: world > 1 needs owner[]");
+  BAM_CHECK_ARG(p.k_row && p.q_gid && p.row_cnt && p.row_off && p.row_tiles && p.row_tiles_asc &&
+                    p.col_cnt && p.col_off && p.col_tiles && p.fwd_order && p.bwd_order &&
+                    p.slot_kb && p.slot_cnt && p.slot_off && p.slot_tiles && p.pair_shared &&
+                    p.fwd_slot_q && p.fwd_slot_cnt && p.fwd_slot_off && p.fwd_slot_tiles &&
+                    p.fwd_shared && p.fwd_pair_ids && p.fwd_rest_items && p.counts,
+                "bam_plan_build: null output buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = p.nb, nq = p.nq;
+  layout_kernel<<<p.world, 1024, 0, s>>>(p.world > 1 ? p.owner : nullptr, nb, p.max_blocks, p.rank,
+                                         p.k_row, p.q_gid);
+  BAM_LAUNCH_CHECK();
+  // tile lists: counts, offsets, ascending rows and columns
+  BAM_CUDA_TRY(cudaMemsetAsync(p.col_cnt, 0, sizeof(int32_t) * nb, s));
+  list_count_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.row_cnt, p.col_cnt);
+  scan_kernel<<<1, 1024, 0, s>>>(p.row_cnt, nq, p.row_off);
+  scan_kernel<<<1, 1024, 0, s>>>(p.col_cnt, nb, p.col_off);
+  list_fill_rows_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, p.row_off, p.row_tiles_asc,
+                                           nullptr, 0);
+  list_fill_cols_kernel<<<nb, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.col_off, p.col_tiles);
+  BAM_LAUNCH_CHECK();
+  // heavy-first orders (LPT's sort key: -count, then index)
+  if (int rc = heavy_first(p.col_cnt, nb, p.bwd_order, s)) return rc;
+  if (int rc = heavy_first(p.row_cnt, nq, p.fwd_order, s)) return rc;
+  // backward CTA-pair step lists over the columns
+  const int bp = (nb + 1) / 2;
+  bwd::pair_lists_kernel<<<(bp + 127) / 128, 128, 0, s>>>(p.col_off, p.col_tiles, p.bwd_order, nb,
+                                                          p.slot_kb, p.slot_cnt, nullptr, nullptr,
+                                                          p.pair_shared);
+  scan_kernel<<<1, 1024, 0, s>>>(p.slot_cnt, 2 * bp, p.slot_off);
+  bwd::pair_lists_kernel<<<(bp + 127) / 128, 128, 0, s>>>(p.col_off, p.col_tiles, p.bwd_order, nb,
+                                                          p.slot_kb, p.slot_cnt, p.slot_off,
+                                                          p.slot_tiles, p.pair_shared);
+  // forward query-block pairs over the (ascending) rows
+  const int fp = (nq + 1) / 2;
+  bwd::pair_lists_kernel<<<(fp + 127) / 128, 128, 0, s>>>(p.row_off, p.row_tiles_asc, p.fwd_order,
+                                                          nq, p.fwd_slot_q, p.fwd_slot_cnt,
+                                                          nullptr, nullptr, p.fwd_shared);
+  scan_kernel<<<1, 1024, 0, s>>>(p.fwd_slot_cnt, 2 * fp, p.fwd_slot_off);
+  bwd::pair_lists_kernel<<<(fp + 127) / 128, 128, 0, s>>>(p.row_off, p.row_tiles_asc, p.fwd_order,
+                                                          nq, p.fwd_slot_q, p.fwd_slot_cnt,
+                                                          p.fwd_slot_off, p.fwd_slot_tiles,
+                                                          p.fwd_shared);
+  fwd_pairs_kernel<<<1, 1024, 0, s>>>(p.fwd_shared, p.fwd_slot_q, p.row_cnt, fp, p.fwd_pair_ids,
+                                      reinterpret_cast<int4*>(p.fwd_rest_items), p.counts);
+  BAM_LAUNCH_CHECK();
+  // the kernels' rows: this rank's key blocks first (CP overlap)
+  if (p.row_tiles != p.row_tiles_asc) {
+    list_fill_rows_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, p.row_off, p.row_tiles,
+                                             p.world > 1 ? p.owner : nullptr, p.rank);
+    BAM_LAUNCH_CHECK();
+  }
+  return kOk;
+}

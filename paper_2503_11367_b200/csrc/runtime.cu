@@ -79,7 +79,16 @@ extern "C" {
 
 const char* bam_last_error(void) { return g_last_error; }
 
-int bam_version(void) { return 1; }
+int bam_version(void) { return 2; }
+
+int64_t bam_sizeof(const char* name) {
+  if (name == nullptr) return -1;
+  if (!strcmp(name, "BamBlockSummary")) return sizeof(BamBlockSummary);
+  if (!strcmp(name, "BamAttnFwdParams")) return sizeof(BamAttnFwdParams);
+  if (!strcmp(name, "BamAttnBwdParams")) return sizeof(BamAttnBwdParams);
+  if (!strcmp(name, "BamPlan")) return sizeof(BamPlan);
+  return -1;
+}
 
 int bam_ilp_optimal(const int64_t* w, int32_t n, int32_t G, int32_t* assignment,
                     int64_t* makespan) {

@@ -31,10 +31,11 @@ def test_library_exports_every_header_symbol():
 def test_struct_sizes_match_header():
     from paper_2503_11367_b200 import _lib
 
+    lib = _lib.load()
     assert ctypes.sizeof(_lib.BamBlockSummary) == 40
-    # pointers + 5 int32 + float + 2 int32 (head group), 8-byte aligned
-    assert ctypes.sizeof(_lib.BamAttnFwdParams) == 11 * 8 + 8 * 4 + 3 * 8 + 2 * 4 + 8 + 4 * 4
-    assert ctypes.sizeof(_lib.BamAttnBwdParams) == 17 * 8 + 8 * 4 + 8 + 2 * 4 + 8 + 2 * 4 + 8 + 2 * 4
+    for name in ("BamBlockSummary", "BamAttnFwdParams", "BamAttnBwdParams", "BamPlan"):
+        assert lib.bam_sizeof(name.encode()) == ctypes.sizeof(getattr(_lib, name)), name
+    assert lib.bam_sizeof(b"nope") == -1
 
 
 def test_ilp_host_entry_point():

@@ -347,3 +347,91 @@ def test_cp_emulated_world8_config4_overlapped_forward():
         assert rel_l2(dq[sl], dq_ref) < 1e-2
     assert rel_l2(dk_sum, dk_1) < 1e-2 and (dk_sum - dk_1).abs().max().item() < 2e-2
     assert rel_l2(dv_sum, dv_1) < 1e-2 and (dv_sum - dv_1).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("policy,world", [("lpt", 1), ("lpt", 4), ("zigzag", 3), ("lpt", 8)])
+def test_native_planner_matches_host_statement(policy, world):
+    """bam_plan_build (one launch sequence, no host sync) against a host
+    restatement with torch/Python of every list it builds: the gathered
+    layout (cp.cp_layout), CSR rows (ascending, and this rank's key blocks
+    first under CP), CSC columns, heavy-first orders (stable sort by -count),
+    the CTA-pair step lists (bam_build_pair_lists) and the forward pair /
+    whole-row item compaction with its device counts."""
+    from paper_2503_11367_b200 import _lib
+    from paper_2503_11367_b200 import cp
+    from paper_2503_11367_b200 import mask as M
+    from paper_2503_11367_b200.workloads import emu_interleave
+
+    mask = M.build_bitfield(emu_interleave(64 * 1024, seed=3))
+    desc = mask.device_descriptors()
+    dev = desc.device
+    cls = None
+    for rank in range(world):
+        plan = cp.make_cp_plan(desc, world, rank, policy)
+        at, lay = plan.attn, plan.layout
+        if cls is None:
+            cls = at.classes.cpu().numpy()
+        nb = at.nb
+        ref = cp.cp_layout(plan.assignment.owner, world, rank)
+        assert torch.equal(lay.k_row.cpu(), ref.k_row.cpu())
+        assert torch.equal(lay.local_blocks.cpu(), ref.local_blocks.cpu())
+        assert lay.counts == ref.counts and lay.max_blocks == ref.max_blocks
+        owner = plan.assignment.owner.cpu().numpy()
+        q_gid = at.q_gid.cpu().numpy()
+        row_off = at.row_off.cpu().numpy()
+        rows = at.row_tiles.cpu().numpy()
+        for j, b in enumerate(q_gid):
+            kbs = np.nonzero(cls[b])[0]
+            exp = [(kb << 2) | cls[b, kb] for kb in kbs]
+            if world > 1:   # this rank's key blocks first, each group ascending
+                exp = ([e for e in exp if owner[e >> 2] == rank] +
+                       [e for e in exp if owner[e >> 2] != rank])
+            assert rows[row_off[j]:row_off[j + 1]].tolist() == exp
+        col_off = at.col_off.cpu().numpy()
+        cols = at.col_tiles.cpu().numpy()
+        sub = cls[q_gid]                                  # [nq, nb]
+        for kb in range(0, nb, 7):
+            js = np.nonzero(sub[:, kb])[0]
+            assert cols[col_off[kb]:col_off[kb + 1]].tolist() == [(j << 2) | sub[j, kb]
+                                                                  for j in js]
+        row_cnt = torch.from_numpy(np.diff(row_off)).to(torch.int64)
+        col_cnt = torch.from_numpy(np.diff(col_off)).to(torch.int64)
+        assert torch.equal(at.fwd_order.cpu().long(), torch.sort(-row_cnt, stable=True).indices)
+        assert torch.equal(at.bwd_order.cpu().long(), torch.sort(-col_cnt, stable=True).indices)
+        # step lists: the standalone bam_build_pair_lists over the same columns
+        npairs = (nb + 1) // 2
+        slot_kb = torch.empty(2 * npairs, dtype=torch.int32, device=dev)
+        slot_cnt, slot_off = torch.empty_like(slot_kb), torch.empty(2 * npairs + 1,
+                                                                    dtype=torch.int32, device=dev)
+        shared = torch.empty(npairs, dtype=torch.int32, device=dev)
+        _lib.call("bam_build_pair_lists", at.col_off.data_ptr(), at.col_tiles.data_ptr(),
+                  at.bwd_order.data_ptr(), nb, slot_kb.data_ptr(), slot_cnt.data_ptr(),
+                  slot_off.data_ptr(), None, shared.data_ptr())
+        n_slot = int(slot_off[-1])
+        tiles = torch.empty(max(n_slot, 1), dtype=torch.int32, device=dev)
+        _lib.call("bam_build_pair_lists", at.col_off.data_ptr(), at.col_tiles.data_ptr(),
+                  at.bwd_order.data_ptr(), nb, slot_kb.data_ptr(), slot_cnt.data_ptr(),
+                  slot_off.data_ptr(), tiles.data_ptr(), shared.data_ptr())
+        assert torch.equal(at.slot_kb, slot_kb) and torch.equal(at.slot_off, slot_off)
+        assert torch.equal(at.pair_shared, shared)
+        assert torch.equal(at.slot_tiles[:n_slot], tiles[:n_slot])
+        # forward pairs -> shared pair ids + whole-row items of the other blocks
+        fsh = None
+        nq = len(q_gid)
+        fp = (nq + 1) // 2
+        fslot = at.fwd_slot_q.cpu().view(fp, 2)
+        # recompute the shared flags from the union rule (8 u <= 9 max) on the rows
+        asc = [sorted(rows[row_off[j]:row_off[j + 1]].tolist()) for j in range(nq)]
+        fsh = []
+        for pr in range(fp):
+            a, b = fslot[pr].tolist()
+            la = {e >> 2 for e in asc[a]} if a >= 0 else set()
+            lb = {e >> 2 for e in asc[b]} if b >= 0 else set()
+            mx = max(len(la), len(lb))
+            fsh.append(b >= 0 and mx > 0 and 8 * len(la | lb) <= 9 * mx)
+        n_pairs, n_rest = at.counts.cpu().tolist()
+        assert at.fwd_pair_ids[:n_pairs].cpu().tolist() == [pr for pr in range(fp) if fsh[pr]]
+        rest = [j for pr in range(fp) if not fsh[pr] for j in fslot[pr].tolist() if j >= 0]
+        assert n_rest == len(rest)
+        items = at.fwd_rest_items[:n_rest].cpu().tolist()
+        assert items == [[j, 0, int(row_cnt[j]), -1] for j in rest]
