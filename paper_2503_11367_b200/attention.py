@@ -95,11 +95,13 @@ def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, n
     sizes = _plan_sizes(nb, nq, n_tiles)
     if world == 1:
         sizes.pop("row_tiles_asc")            # one buffer: the rows are ascending either way
-    ws = torch.empty(sum(sizes.values()), dtype=torch.int32, device=classes.device)
+    pad = lambda n: -(-n // 64) * 64            # noqa: E731  256-B aligned views (int4 items)
+    ws = torch.empty(sum(pad(n) for n in sizes.values()), dtype=torch.int32,
+                     device=classes.device)
     views, off = {}, 0
     for name, n in sizes.items():
         views[name] = ws[off:off + n]
-        off += n
+        off += pad(n)
     if world == 1:
         views["row_tiles_asc"] = views["row_tiles"]
     bp = _lib.BamPlan(classes.data_ptr(), owner.data_ptr() if owner is not None else None, nb,

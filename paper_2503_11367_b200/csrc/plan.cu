@@ -151,6 +151,8 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
                     p.fwd_slot_q && p.fwd_slot_cnt && p.fwd_slot_off && p.fwd_slot_tiles &&
                     p.fwd_shared && p.fwd_pair_ids && p.fwd_rest_items && p.counts,
                 "bam_plan_build: null output buffer");
+  BAM_CHECK_ARG(((uintptr_t)p.fwd_rest_items & 15) == 0,
+                "bam_plan_build: fwd_rest_items must be 16-byte aligned (int4 records)");
   cudaStream_t s = (cudaStream_t)stream;
   const int nb = p.nb, nq = p.nq;
   layout_kernel<<<p.world, 1024, 0, s>>>(p.world > 1 ? p.owner : nullptr, nb, p.max_blocks, p.rank,
