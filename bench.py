@@ -489,8 +489,6 @@ def main():
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_fwd[b])
                 h_outs[b][0].copy_(o.detach(), non_blocking=True)
-            if fresh_plan and s + 1 < n:
-                prepare(s + 1)            # the next batch's mask + plan, under this step
             cur.wait_event(ev_do[b])
             o.backward(dod)
             outs = (qd.grad, kd.grad, vd.grad)
@@ -501,6 +499,10 @@ def main():
                     dst.copy_(src, non_blocking=True)
                     src.record_stream(s_out)
                 o.record_stream(s_out)
+            if fresh_plan and s + 1 < n:
+                # the next batch's mask + plan, once this step's backward is queued: the
+                # host's one sync (plan stream only) then overlaps the backward
+                prepare(s + 1)
         cur.wait_stream(s_out)
         cur.wait_stream(plan_stream)
 
@@ -603,7 +605,8 @@ def main():
                         "value": e2e_fresh_value, "ms_per_step": e2e_fresh_ms,
                         "what": "every step runs on a plan from a freshly built mask "
                                 "(build_bitfield + make_cp_plan), prepared one step ahead on a "
-                                "high-priority planning stream under the previous step"}},
+                                "high-priority planning stream while the previous step's "
+                                "backward runs"}},
             "planning": planning,
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -11,8 +11,8 @@ step reuses the exchange buffers), and checks ITS OWN rows:
 
 * O and dQ of sampled local query blocks (first, heaviest, last) against the
   fp32 CPU oracle (those rows against all keys);
-* dK/dV of the last key block if this rank owns it (only the last query
-  block sees it, so the oracle is cheap) against the oracle;
+* dK/dV of the owned key block that the fewest query blocks see (the
+  oracle needs only those rows) against the oracle;
 * every local row of O/dQ and every owned row of dK/dV against the
   single-GPU path (``bitfield_attention`` on the whole sequence, itself
   oracle-checked at this size by tests/test_gpu_large.py) -- the exchange
@@ -110,17 +110,22 @@ def main():
     record("O_oracle_sampled", o_loc[rl], o_ref)
     record("dQ_oracle_sampled", dq_loc[rl], dq_ref)
 
-    # (2) oracle dK/dV of the last key block (seen by the last query block only)
-    pos = np.nonzero(local == nb - 1)[0]
-    if pos.size:
-        i = int(pos[0])
-        rows = np.arange((nb - 1) * 128, nb * 128)
+    # (2) oracle dK/dV of the owned key block seen by the fewest query blocks: the
+    # oracle needs only those query rows (their full softmax rows), not all 128K
+    cls = plan.attn.classes.cpu().numpy()
+    seen = (cls != 0).sum(axis=0)
+    i = int(np.argmin(seen[local]))
+    kb = int(local[i])
+    qbs = np.nonzero(cls[:, kb])[0]
+    if len(qbs) <= 8:
+        rows = np.concatenate([np.arange(b * 128, (b + 1) * 128) for b in qbs])
         rt = torch.from_numpy(rows)
         o_r, lse_r = attention_ref.attention_fwd(q[rt], k, v, desc, rows, chunk=128)
         _, dk_r, dv_r = attention_ref.attention_bwd(q[rt], k, v, o_r, lse_r, do[rt], desc, rows,
                                                     chunk=128)
-        record("dK_oracle_last_block", dk_loc[i * 128:(i + 1) * 128], dk_r[rt])
-        record("dV_oracle_last_block", dv_loc[i * 128:(i + 1) * 128], dv_r[rt])
+        kr = torch.arange(kb * 128, (kb + 1) * 128)
+        record(f"dK_oracle_block{kb}_seen_by_{len(qbs)}", dk_loc[i * 128:(i + 1) * 128], dk_r[kr])
+        record(f"dV_oracle_block{kb}_seen_by_{len(qbs)}", dv_loc[i * 128:(i + 1) * 128], dv_r[kr])
 
     # (3) every local / owned row against the single-GPU path
     full = [t.clone().requires_grad_(True) for t in (qd, kd, vd)]

@@ -302,6 +302,10 @@ def test_cp_emulated_world8_config4_overlapped_forward():
         v_src[:, idx] = vd.transpose(0, 1)
         k_all[:, mine] = k_src[:, mine]          # this rank's rows: present at launch
         v_all[:, mine] = v_src[:, mine]
+        # the peers' rows arrive by DMA (pinned host -> device, a copy engine, like the
+        # NVLink pulls): the spinning forward CTAs occupy every SM, so a copy that
+        # needed an SM (a same-device D2D copy kernel) could never run
+        k_src_h, v_src_h = k_src.cpu().pin_memory(), v_src.cpu().pin_memory()
         flags = torch.zeros(world * Hkv, dtype=torch.int32, device=dev)
         epoch = 3 + rank
         q_loc, do_loc = cp.shard_rows(qd, dod, layout=lay)
@@ -313,8 +317,8 @@ def test_cp_emulated_world8_config4_overlapped_forward():
                     continue
                 sl = slice(peer * rows, (peer + 1) * rows)
                 for h in range(Hkv):
-                    k_all[h, sl].copy_(k_src[h, sl])
-                    v_all[h, sl].copy_(v_src[h, sl])
+                    k_all[h, sl].copy_(k_src_h[h, sl], non_blocking=True)
+                    v_all[h, sl].copy_(v_src_h[h, sl], non_blocking=True)
                     _lib.call("bam_stream_write_i32", flags[peer * Hkv + h:].data_ptr(), epoch)
         o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn,
                                 kv_ready=(flags, epoch, rank, lay.max_blocks), kv_head_major=True)
