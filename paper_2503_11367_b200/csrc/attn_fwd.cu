@@ -88,6 +88,12 @@ __device__ __forceinline__ WorkItem work_item(const BamAttnFwdParams& p, int y) 
 #define BAM_FWD_ROW_MAJOR 1
 #endif
 constexpr bool kRowMajor = BAM_FWD_ROW_MAJOR;
+// P(t) released to the PV MMAs in chunks (2: keys 32 apart per thread half; 4: 16).
+// Measured on config 4: one release 1210, 2 chunks 1320-1330 TFLOP/s
+#ifndef BAM_FWD_P_CHUNKS
+#define BAM_FWD_P_CHUNKS 2
+#endif
+constexpr int kPChunks = BAM_FWD_P_CHUNKS;
 
 template <int kPolyEvery>
 __device__ __forceinline__ void softmax_role(const BamAttnFwdParams& p, uint32_t tmem,
@@ -398,8 +404,9 @@ constexpr int kPairThreads = 320;   // the CTA-pair kernel's block size
 template <int kPolyEvery>
 __device__ __forceinline__ void softmax_half_role(
     const BamAttnFwdParams& p, uint32_t tmem, uint32_t colS, uint32_t colO, uint64_t* bar_s_full,
-    uint64_t* bar_p_ready, uint64_t* bar_pv_done, int j, int h, uint32_t lw, uint32_t lane,
-    const int32_t* tiles, int n, int slot, float* xch /* [2][2][128] */, uint32_t bar_id) {
+    uint64_t* bar_p_ready /* [2]: P chunk 0, 1 */, uint64_t* bar_pv_done, int j, int h,
+    uint32_t lw, uint32_t lane, const int32_t* tiles, int n, int slot,
+    float* xch /* [2][2][128] */, uint32_t bar_id) {
   const uint32_t q = lw & 3, hf = lw >> 2;
   const int r = q * 32 + lane;
   const uint32_t lane_base = (q * 32) << 16;
@@ -467,38 +474,49 @@ __device__ __forceinline__ void softmax_half_role(
     const float mb = (m == -INFINITY) ? 0.f : m;
     const float2 sc2 = make_float2(scale_log2, scale_log2), nmb2 = make_float2(-mb, -mb);
     float2 ls = make_float2(0.f, 0.f);
+    // P in kPChunks key chunks per thread (keys [64 hf + c 64/kPChunks, ...)), each
+    // released on its own barrier: the MMA warp starts PV on the first chunks while
+    // the later chunks' exponentials are still running
+    constexpr int kPairsPerChunk = 32 / kPChunks;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t pk[16];
+    for (int c = 0; c < kPChunks; ++c) {
+      uint32_t pk[kPairsPerChunk];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float2 x = ffma2(make_float2(__uint_as_float(sr[c * 32 + 2 * i]),
-                                           __uint_as_float(sr[c * 32 + 2 * i + 1])),
+      for (int i = 0; i < kPairsPerChunk; ++i) {
+        const int i2 = c * kPairsPerChunk + i;   // pair index within the thread's 64 keys
+        const float2 x = ffma2(make_float2(__uint_as_float(sr[2 * i2]),
+                                           __uint_as_float(sr[2 * i2 + 1])),
                                sc2, nmb2);
-        const float2 pp = (kPolyEvery > 0 && (c * 16 + i) % (kPolyEvery > 0 ? kPolyEvery : 1) ==
+        const float2 pp = (kPolyEvery > 0 && i2 % (kPolyEvery > 0 ? kPolyEvery : 1) ==
                                                  kPolyEvery - 1)
                               ? ex2_poly2(x)
                               : make_float2(ex2(x.x), ex2(x.y));
         ls = fadd2(ls, pp);
         pk[i] = pack_bf16(pp.x, pp.y);
       }
-      BAM_TMEM_ST16(tmem + lane_base + cP + c * 16, pk);
+      if constexpr (kPairsPerChunk == 16)
+        BAM_TMEM_ST16(tmem + lane_base + cP + c * 16, pk);
+      else
+        BAM_TMEM_ST8(tmem + lane_base + cP + c * 8, pk);
+      // the lazy rescale of O precedes the release of P(t)'s first chunk (PV(t-1) has
+      // completed: S(t), committed after it by the same thread, is done); here, once
+      // chunk 0's S values are dead, it fits the register budget (16-column pieces)
+      if (c == 0 && __any_sync(0xffffffffu, rescale) && t > 0) {
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t rr[16];
+          BAM_TMEM_LD16(tmem + lane_base + cO + cc * 16, rr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+          BAM_TMEM_ST16(tmem + lane_base + cO + cc * 16, rr);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_p_ready + c);
     }
     l += ls.x + ls.y;
-    if (__any_sync(0xffffffffu, rescale) && t > 0) {
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t rr[32];
-        BAM_TMEM_LD32(tmem + lane_base + cO + c * 32, rr);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
-        BAM_TMEM_ST32(tmem + lane_base + cO + c * 32, rr);
-      }
-    }
-    tmem_wait_st();
-    tc_fence_before();
-    mbar_arrive(bar_p_ready);
   }
   // row sum of both halves (same m in both threads)
   xch[512 + hf * 128 + r] = l;
@@ -574,7 +592,7 @@ struct SplitSmem {
   alignas(1024) uint8_t v[2][kTileBytes];
   float xch[2][768];  // per head: max exchange [2 parity][2 halves][128] + row sums [2][128]
   uint64_t bar_q, bar_k_full[2], bar_k_empty[2], bar_v_full[2], bar_v_empty[2];
-  uint64_t bar_s_full[2], bar_p_ready[2], bar_pv_done[2];
+  uint64_t bar_s_full[2], bar_p_ready[2][kPChunks], bar_pv_done[2];  // p_ready[head][chunk]
   uint32_t tmem_base;
 };
 
@@ -631,7 +649,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
       mbar_init(&sm.bar_v_full[i], 1);
       mbar_init(&sm.bar_v_empty[i], 1);
       mbar_init(&sm.bar_s_full[i], 1);
-      mbar_init(&sm.bar_p_ready[i], 256);
+      for (int c = 0; c < kPChunks; ++c) mbar_init(&sm.bar_p_ready[i][c], 256);
       mbar_init(&sm.bar_pv_done[i], 1);
     }
     fence_mbar_init();
@@ -702,12 +720,23 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         }
         tc_commit_w(&sm.bar_s_full[i], leader);
       };
+      // PV(t) of head i in kPChunks parts as the softmax releases the P chunks: chunk c
+      // covers the 16-key MMA steps kk = hf 4 + c (4 / kPChunks) + u of both thread
+      // halves hf
       auto issue_pv = [&](int i, int t) {
         const uint64_t dv = dv0 + (t & 1) * kTile16;
+        constexpr int kKPer = 4 / kPChunks;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts_w(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, dv + kk * 128, idesc_o,
-                   (t > 0 || kk > 0), leader);
+        for (int c = 0; c < kPChunks; ++c) {
+          mbar_wait(&sm.bar_p_ready[i][c], t & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int u = 0; u < 2 * kKPer; ++u) {
+            const int kk = (u / kKPer) * 4 + c * kKPer + u % kKPer;
+            mma_ts_w(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, dv + kk * 128, idesc_o,
+                     (t > 0 || c > 0 || u > 0), leader);
+          }
+        }
         tc_commit_w(&sm.bar_pv_done[i], leader);
       };
       mbar_wait(&sm.bar_q, 0);
@@ -718,17 +747,13 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
       tc_commit_w(&sm.bar_k_empty[0], leader);
       for (int t = 0; t < n; ++t) {
         const int st = t & 1, st1 = (t + 1) & 1;
-        mbar_wait(&sm.bar_p_ready[0], t & 1);
         mbar_wait(&sm.bar_v_full[st], (t >> 1) & 1);
-        tc_fence_after();
         issue_pv(0, t);
         if (t + 1 < n) {
           mbar_wait(&sm.bar_k_full[st1], ((t + 1) >> 1) & 1);
           tc_fence_after();
           issue_s(0, t + 1);
         }
-        mbar_wait(&sm.bar_p_ready[1], t & 1);
-        tc_fence_after();
         issue_pv(1, t);
         tc_commit_w(&sm.bar_v_empty[st], leader);
         if (t + 1 < n) {
@@ -741,7 +766,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     const int i = warp >> 3;  // head: warps 0-7 / 8-15
     const uint32_t lw = warp & 7;
     softmax_half_role<BAM_FWD_POLY_SPLIT>(p, tmem, 128 * i, 256 + 128 * i, &sm.bar_s_full[i],
-                                          &sm.bar_p_ready[i], &sm.bar_pv_done[i], jj[i], hh[i],
+                                          sm.bar_p_ready[i], &sm.bar_pv_done[i], jj[i], hh[i],
                                           lw, lane, tl[i], n, slot, sm.xch[i],
                                           1 + i * 4 + (lw & 3));
   }
