@@ -217,14 +217,8 @@ typedef struct BamAttnBwdParams {
    * tile to both CTAs (each loads one half). */
   const int32_t* pair_shared;
   int32_t n_slots, pad_;
-  /* Optional CP reduce-scatter overlap: head_done[hkv] is incremented (after a
-   * GPU-scope fence) by every CTA of KV head hkv when it has written its dK/dV
-   * rows, so a stream waiting for head_done[h] >= CTAs per head (grid.x) can
-   * ship head h while the kernel still runs.  dkv_head_major != 0: dk / dv are
-   * [Hkv, k_rows*128, 128] (each head's partials contiguous). */
-  int32_t* head_done;
-  int32_t dkv_head_major;
   int32_t kv_head_major;    /* k/v head-major [Hkv, k_rows*128, 128] */
+  int32_t pad2_;
   /* Optional CP reduce-scatter fused into the epilogue: when dkv_peers != NULL
    * (a DEVICE array of one pointer per rank, each the UVA address of this
    * rank's slot [2][Hkv][dkv_rows_per_owner][128] fp32 in that rank's
@@ -309,7 +303,7 @@ int bam_plan_build(const BamPlan* plan, void* stream);
  * BamAttnFwdParams.kv_ready. */
 int bam_stream_write_i32(int32_t* dst, int32_t value, void* stream);
 /* Stream-ordered wait (cuStreamWaitValue32, GEQ): the stream's later work
- * starts once *src >= value (the backward's head_done counters). */
+ * starts once *src >= value (no SM involved). */
 int bam_stream_wait_i32_geq(const int32_t* src, int32_t value, void* stream);
 
 /* ---- token permutation ----------------- */

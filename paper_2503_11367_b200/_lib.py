@@ -56,7 +56,7 @@ class BamAttnBwdParams(ctypes.Structure):
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("pair_shared", c_vp), ("n_slots", c_i32), ("pad_", c_i32),
-                ("head_done", c_vp), ("dkv_head_major", c_i32), ("kv_head_major", c_i32),
+                ("kv_head_major", c_i32), ("pad2_", c_i32),
                 ("dkv_peers", c_vp), ("dkv_rows_per_owner", c_i32), ("pad3_", c_i32)]
 
 

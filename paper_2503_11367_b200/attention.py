@@ -341,12 +341,8 @@ class BackwardWorkspace:
     def _pairs(self) -> bool:
         return self.plan.pair_shared is not None and os.environ.get("BAM_BWD_PAIRS", "1") != "0"
 
-    def ctas_per_head(self) -> int:
-        """CTAs of the main kernel per KV head (what head_done[h] counts up to)."""
-        return int(self.plan.slot_kb.shape[0]) if self._pairs() else self.plan.nb
-
-    def _params(self, k, v, dk, dv, h_begin, nh, Hkv, head_done=None, head_major=False,
-                kv_head_major=False, dkv_peers=None, rows_per_owner=0):
+    def _params(self, k, v, dk, dv, h_begin, nh, Hkv, kv_head_major=False, dkv_peers=None,
+                rows_per_owner=0):
         pl = self.plan
         pairs = self._pairs()
         col_off, col_tiles, order = ((pl.slot_off, pl.slot_tiles, pl.slot_kb) if pairs else
@@ -360,23 +356,19 @@ class BackwardWorkspace:
             col_tiles.data_ptr(), order.data_ptr(), pl.nq, pl.nb, pl.k_rows,
             self.q.shape[1], Hkv, self.scale, h_begin, nh,
             pl.pair_shared.data_ptr() if pairs else None,
-            int(pl.slot_kb.shape[0]) if pairs else 0, 0,
-            head_done.data_ptr() if head_done is not None else None, int(head_major),
-            int(kv_head_major), dkv_peers.data_ptr() if dkv_peers is not None else None,
-            int(rows_per_owner), 0)
+            int(pl.slot_kb.shape[0]) if pairs else 0, 0, int(kv_head_major), 0,
+            dkv_peers.data_ptr() if dkv_peers is not None else None, int(rows_per_owner), 0)
 
     def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv, **kw):
         _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv, **kw))
 
-    def main(self, k, v, *, h_begin=0, nh=0, timer=None, head_done=None, head_major=False,
-             kv_head_major=False, dkv_peers=None, rows_per_owner=0):
-        """dK/dV fp32 partials of the head group, [k_rows*128, Hkv, 128] (or
-        [Hkv, k_rows*128, 128] with head_major); dQ accumulates.  head_done
-        (int32 [Hkv], zeroed): per-KV-head CTA completion counters.
-        kv_head_major: k/v are [Hkv, k_rows*128, 128].  dkv_peers (int64 device
-        tensor of per-rank workspace-slot addresses) with rows_per_owner: the
-        partials go straight to their owners (fused reduce-scatter); returns
-        (None, None)."""
+    def main(self, k, v, *, h_begin=0, nh=0, timer=None, kv_head_major=False, dkv_peers=None,
+             rows_per_owner=0):
+        """dK/dV fp32 partials of the head group, [k_rows*128, Hkv, 128]; dQ
+        accumulates.  kv_head_major: k/v are [Hkv, k_rows*128, 128].
+        dkv_peers (int64 device tensor of per-rank workspace-slot addresses)
+        with rows_per_owner: the partials go straight to their owners (fused
+        reduce-scatter); returns (None, None)."""
         rows = self.plan.k_rows * BLOCK
         if kv_head_major:
             Hkv = _check_kv_head_major(k, v, self.plan)
@@ -388,13 +380,12 @@ class BackwardWorkspace:
         if dkv_peers is not None:
             dk = dv = None
         else:
-            shape = (Hkv, rows, HEAD_DIM) if head_major else (rows, Hkv, HEAD_DIM)
-            dk = torch.empty(shape, dtype=torch.float32, device=k.device)
-            dv = torch.empty(shape, dtype=torch.float32, device=k.device)
+            dk = torch.empty((rows, Hkv, HEAD_DIM), dtype=torch.float32, device=k.device)
+            dv = torch.empty((rows, Hkv, HEAD_DIM), dtype=torch.float32, device=k.device)
         if timer is not None:
             timer[0].record()
-        self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv, head_done=head_done,
-                   head_major=head_major, kv_head_major=kv_head_major, dkv_peers=dkv_peers,
+        self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv,
+                   kv_head_major=kv_head_major, dkv_peers=dkv_peers,
                    rows_per_owner=rows_per_owner)
         if timer is not None:
             timer[1].record()

@@ -6,35 +6,36 @@
 // predicate of mask.py:106-112 in registers), for every query head of the
 // GQA group.  A step is one 64-row half of a query block for one head
 // (j outer, head, half inner, so CTAs running together hit the same dQ
-// accumulator lines in L2):
-// Default (BAM_BWD_KVT = 1): K and V are copied into TMEM once per CTA and are
-// the A operands of the TS MMAs
+// accumulator lines in L2).  K and V are copied into TMEM once per CTA and
+// are the A operands of the TS MMAs:
 //   S^T  = K Q^T      (TS, M=128 keys, N=64)  -> TMEM S        P^T = exp2(S^T c - LSE)
 //                     (P^T bf16 of queries [32c, 32c+32) over S cols [32c, 32c+16))
 //   dP^T = V dO^T     (TS)                    -> TMEM dP       dS^T = P^T (dP^T - D)
 //   dV  += P^T dO     (TS: P^T bf16 in S, dO MN-major)         -> TMEM [0,128)
 //   dK  += dS^T Q     (SS: dS^T K-major in smem, Q MN-major)   -> TMEM [128,256)
 //   dQ^T = K^T dS^T   (SS: K MN-major, dS^T MN-major)          -> TMEM dP
-// with S / dP single-buffered: S(s+1) is issued right after dV(s) so it runs
-// while the compute warps turn dP(s) into dS(s).  The all-SS variant
-// (BAM_BWD_KVT = 0) double-buffers S_b / dP_b instead (b = step & 1) and keeps
-// dS^T in TMEM for a TS dK.  dQ^T puts d on the TMEM lanes; the dQ warps stage
-// each 64-query dQ^T tile (32 KB fp32) in shared memory (two stages: the freed V
-// region and one more) and one TMA bulk reduce-add adds it into the head-major
-// accumulator.  Q/dO half tiles (+ the (lse, D) pairs) stream through a 3-stage
-// TMA ring.
+// with S / dP single-buffered (TMEM holds dV, dK, K, V, S, dP = 512 columns):
+// S(s+1) is issued right after dV(s) so it runs while the compute warps turn
+// dP(s) into dS(s), and P^T(s) reaches dV(s) in two chunks.  dQ^T puts d on
+// the TMEM lanes; the dQ warps stage each 64-query dQ^T tile (32 KB fp32) in
+// shared memory (two stages: the freed V region and one more, so the drain
+// never waits for the previous bulk reduce) and one TMA bulk reduce-add adds
+// it into the head-major accumulator.  Q/dO half tiles (+ the (lse, D) pairs)
+// stream through a 3-stage TMA ring.
 // Warp roles (448 threads, 1 CTA / SM):
 //   warps 0-7 compute (two warpgroups, 32 query columns each; thread r = key
 //   row r), warps 8-11 dQ epilogue (thread r = head-dim column r), warp 12
 //   MMA issuer + TMEM alloc, warp 13 TMA producer (Q/dO half tiles + LSE/D).
 // CTA pairs (clusters of 2 along the slot axis) whose key blocks share one
 // step list multicast each Q/dO stage to both CTAs.
-// Bounds (profiles/r01/bwd_variants.md): the fp32 dQ reduce-adds
-// into L2 (357 GB per config-4 launch) run at ~3.6 TB/s device-wide; shared
-// memory feeds 128 B/clk (~224 KB per step here, 288 KB in the all-SS variant).
-// Compile-time variants kept for the measurements there: BAM_DQ_MODE,
-// BAM_BWD_KVT, BAM_BWD_SLOT_MAJOR, BAM_BWD_POLY_EVERY, and the development
-// aids BAM_TRACE, BAM_EXPERIMENT_MMA_ONLY, BAM_EXPERIMENT_NO_DQ_RED.
+// Bounds (profiles/r01/bwd_variants.md, profiles/r02/): the fp32
+// dQ reduce-adds into L2 (357 GB per config-4 launch), the shared-memory port
+// (128 B/clk: MMA operands, TMA writes, dS^T and dQ staging) and the
+// single-buffered S/dP chain.  Alternatives measured slower and removed: the
+// all-SS double-buffered kernel (975-985 vs 1075 TFLOP/s), dQ by red.global
+// from registers (931-956 / 891-896), the CTA-pair DSMEM dQ sum (469-523), lse/D
+// by warp shuffles instead of broadcast loads (-2%).  BAM_TRACE builds record
+// per-step events for tools/trace_bwd.py.
 #include "../../include/bam.h"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -47,58 +48,22 @@ namespace bwd {
 constexpr int kThreads = 448;
 // warp roles
 constexpr uint32_t kWarpDQ = 8, kWarpMMA = 12, kWarpTMA = 13;
-// How dQ^T tiles reach the fp32 accumulator:
-//   0: 64 per-thread red.global.add.f32 per step (one 128-B row segment per warp op)
-//   1: staged in shared memory, one 32-KB TMA bulk reduce-add (costs a Q/dO stage)
-//   2: 4x4 quad transposes in registers, 16 red.global.add.v4.f32 per thread
-//      (512 B per warp op, no shared-memory traffic)
-#ifndef BAM_DQ_MODE
-#define BAM_DQ_MODE 1
-#endif
-#define BAM_DQ_BULK (BAM_DQ_MODE == 1)
-// 1: K and V resident in TMEM as the A operands of S^T / dP^T (TS MMAs), dK from
-// dS^T in shared memory: per step the MMAs read 128 KB of shared memory instead
-// of 176 KB (an SS MMA with N = 64 is shared-memory bound at 48 clk per k-step,
-// a TS one runs at the 32-clk tensor rate: tools/mma_bench.cu), at the price of
-// single-buffered S / dP, which puts the softmax / dS work on the MMA chain.
-// Measured on config 4: MMA pipeline alone 1600 vs 1240 TFLOP/s; with the dQ
-// staging double-buffered (BAM_DQ_STAGE2, so the single-buffered chain never
-// waits on a bulk reduce) the full kernel runs 1020-1038 vs 975-985 TFLOP/s.
-// 1 (default).  0 = double-buffered S / dP, both SS, one 32-KB dQ stage.
-// Backward epilogue through shared memory + bulk copies for local dK/dV too
-// (always for the fused reduce-scatter's peer stores).  Off: measured 0.6%
-// slower than plain stores for local rows (config 4: bwd 106.7 vs 107.3 ms).
-#ifndef BAM_EPI_BULK_LOCAL
-#define BAM_EPI_BULK_LOCAL 0
-#endif
-#ifndef BAM_BWD_KVT
-#define BAM_BWD_KVT 1
-#endif
-// BAM_BWD_KVT: a second 32-KB dQ staging buffer (the first is the V region), so
-// the dQ warps drain TMEM without waiting for the previous bulk reduce to read
-// its buffer (costs a Q/dO stage); the single-buffered S/dP chain needs it.
-#ifndef BAM_DQ_STAGE2
-#define BAM_DQ_STAGE2 (BAM_BWD_KVT && BAM_DQ_BULK)
-#endif
-constexpr int kStages = (BAM_DQ_BULK && (!BAM_BWD_KVT || BAM_DQ_STAGE2)) ? 3 : 4;
+constexpr int kStages = 3;       // Q/dO half-tile ring (the dQ staging takes the 4th slot)
+// P^T(s) reaches the dV MMAs in two chunks of 16 queries per warpgroup
+constexpr int kBwdPChunks = 2;
 #ifndef BAM_DQ_SLEEP_NS
 #define BAM_DQ_SLEEP_NS 64
 #endif
-// Grid order.  Slot-major (key blocks fastest, one KV head after the other):
-// the ~148 CTAs resident together are key blocks of ONE KV head, so their dQ
+// Grid order: slot-major (key blocks fastest, one KV head after the other): the
+// ~148 CTAs resident together are key blocks of ONE KV head, so their dQ
 // reductions land in that head group's quarter-GiB slice of dq_acc, whose
-// active window stays in L2.  Head-major (KV heads fastest) spreads each wave
-// over all eight slices and re-reads dq_acc from DRAM once per wave.
-#ifndef BAM_BWD_SLOT_MAJOR
-#define BAM_BWD_SLOT_MAJOR 1
-#endif
-constexpr bool kSlotMajor = BAM_BWD_SLOT_MAJOR;
+// active window stays in L2 (DRAM traffic per config-4 launch 94 -> 14.8 GB).
 constexpr uint32_t kTileBytes = 128 * 128 * 2;   // K, V: 128 rows x 128 cols (two 64-col boxes)
 constexpr uint32_t kHalfBytes = 64 * 128 * 2;    // Q, dO half tile: 64 rows x 128 cols
 constexpr uint32_t kDsBytes = 128 * 64 * 2;      // dS^T: 128 key rows x 64 query cols
-constexpr uint32_t kColDV = 0, kColDK = 128, kColBuf = 256;  // buffer b: S at 256+128b, dP at +64
-// BAM_BWD_KVT: K, V bf16 pairs (64 columns each), then the single S and dP/dQ^T buffers
-constexpr uint32_t kColK = 256, kColV = 320, kColS = 384, kColDP = 448;
+// TMEM columns: dV, dK accumulators; K, V as bf16 pairs; single S and dP/dQ^T buffers
+constexpr uint32_t kColDV = 0, kColDK = 128, kColK = 256, kColV = 320, kColS = 384,
+                   kColDP = 448;
 
 struct Stage {
   alignas(1024) uint8_t q[kHalfBytes];
@@ -108,98 +73,32 @@ struct Stage {
 struct Smem {
   alignas(1024) uint8_t k[kTileBytes];
   alignas(1024) uint8_t v[kTileBytes];
-  alignas(1024) uint8_t ds[BAM_BWD_KVT ? 1 : 2][kDsBytes];
+  alignas(1024) uint8_t ds[kDsBytes];
   Stage st[kStages];
-#if BAM_DQ_BULK && (!BAM_BWD_KVT || BAM_DQ_STAGE2)
   alignas(128) float dq_stage[64 * 128];  // dQ tile [64 queries][128 d] fp32 for the bulk reduce
-#endif
   alignas(16) float ld[kStages][128];   // per stage: (lse * log2e, delta) pairs, 64 queries
   uint64_t bar_kv, bar_full[kStages], bar_empty[kStages];
-  uint64_t bar_sdp_full[2], bar_p_ready[2], bar_mma_done[2], bar_dq_full[2], bar_dq_empty[2];
-  uint64_t bar_kvt, bar_dp_full, bar_ds_ready;  // BAM_BWD_KVT (S(s) done = bar_sdp_full[0])
+  uint64_t bar_s_full, bar_p_ready[kBwdPChunks], bar_mma_done, bar_dq_full, bar_dq_empty;
+  uint64_t bar_kvt, bar_dp_full, bar_ds_ready;
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void red_add(float* addr, float a) {
-  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
-}
-
-// v[i] = dQ[row0 + i][d] for this lane's column d.  Quads of lanes transpose
-// 4x4 blocks so lane 4m+k holds dQ[q][4m'..4m'+3] for q = row0 + 4t + k, then
-// one 16-B reduction per (t): a warp covers 4 rows x 128 B per instruction.
-__device__ __forceinline__ void red_add_quads(float* base, int d, const uint32_t (&v)[32],
-                                              int row0) {
-  const int k = d & 3, col = (d & ~3) ;   // col: first column of this lane's quad
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    float x0 = __uint_as_float(v[4 * t]), x1 = __uint_as_float(v[4 * t + 1]);
-    float x2 = __uint_as_float(v[4 * t + 2]), x3 = __uint_as_float(v[4 * t + 3]);
-    float s0 = __shfl_xor_sync(0xffffffffu, (k & 1) ? x0 : x1, 1);
-    float s1 = __shfl_xor_sync(0xffffffffu, (k & 1) ? x2 : x3, 1);
-    if (k & 1) { x0 = s0; x2 = s1; } else { x1 = s0; x3 = s1; }
-    s0 = __shfl_xor_sync(0xffffffffu, (k & 2) ? x0 : x2, 2);
-    s1 = __shfl_xor_sync(0xffffffffu, (k & 2) ? x1 : x3, 2);
-    if (k & 2) { x0 = s0; x1 = s1; } else { x2 = s0; x3 = s1; }
-    float* addr = base + (int64_t)(row0 + 4 * t + k) * 128 + col;
-    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "f"(x0), "f"(x1),
-                 "f"(x2), "f"(x3)
-                 : "memory");
-  }
-}
-
-// dst[(kRow0 + i) * 128] += v[i] for i < 32, rows 512 B apart (immediate offsets)
-template <int kRow0, int i = 0>
-__device__ __forceinline__ void red_add_rows(float* dst, const uint32_t (&v)[32]) {
-  if constexpr (i < 32) {
-    asm volatile("red.global.add.f32 [%0+%2], %1;" ::"l"(dst), "f"(__uint_as_float(v[i])),
-                 "n"((kRow0 + i) * 512)
-                 : "memory");
-    red_add_rows<kRow0, i + 1>(dst, v);
-  }
-}
-
-// Development aid: -DBAM_EXPERIMENT_MMA_ONLY runs only the TMA + MMA pipeline
-// (no softmax / dQ work, garbage results) to measure the operand-feed bound.
-#ifdef BAM_EXPERIMENT_MMA_ONLY
-#define BAM_XWAIT(bar, ph) ((void)0)
-constexpr bool kMmaOnly = true;
-#else
-#define BAM_XWAIT(bar, ph) mbar_wait(bar, ph)
-constexpr bool kMmaOnly = false;
-#endif
-
-// P = 2^(S c - lse) for a pair of queries (packed FFMA2), one in kBwdPoly
-// pairs on the FMA pipe (ex2_poly2), masked by the PARTIAL-tile allow bits.
-#ifndef BAM_BWD_POLY_EVERY
-#define BAM_BWD_POLY_EVERY 0
-#endif
-constexpr int kBwdPoly = BAM_BWD_POLY_EVERY;
-// (The all-SS kernel runs at 128 registers and keeps the scalar forms: the
-// register pairs FFMA2 needs make it spill; its softmax is off the MMA chain.)
+// P = 2^(S c - lse) for a pair of queries (packed FFMA2, exponentials on MUFU:
+// the backward's MUFU is ~25% busy, a polynomial share measured slower), masked by
+// the PARTIAL-tile allow bits.
 __device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, float lse0, float lse1,
                                          float sc, int i2, uint32_t allow) {
-#if BAM_BWD_KVT
   const float2 x = ffma2(make_float2(__uint_as_float(s0), __uint_as_float(s1)),
                          make_float2(sc, sc), make_float2(-lse0, -lse1));
-#else
-  const float2 x = make_float2(fmaf(__uint_as_float(s0), sc, -lse0),
-                               fmaf(__uint_as_float(s1), sc, -lse1));
-#endif
-  float2 p = (kBwdPoly > 0 && i2 % (kBwdPoly > 0 ? kBwdPoly : 1) == kBwdPoly - 1)
-                 ? ex2_poly2(x)
-                 : make_float2(ex2(x.x), ex2(x.y));
+  float2 p = make_float2(ex2(x.x), ex2(x.y));
   p.x = (allow >> (2 * i2)) & 1 ? p.x : 0.f;
   p.y = (allow >> (2 * i2 + 1)) & 1 ? p.y : 0.f;
   return p;
 }
 // dS = P (dP - D) for the same pair
 __device__ __forceinline__ float2 ds_pair(float2 p, uint32_t dp0, uint32_t dp1, float D0, float D1) {
-#if BAM_BWD_KVT
   return fmul2(p, fadd2(make_float2(__uint_as_float(dp0), __uint_as_float(dp1)),
                         make_float2(-D0, -D1)));
-#else
-  return make_float2(p.x * (__uint_as_float(dp0) - D0), p.y * (__uint_as_float(dp1) - D1));
-#endif
 }
 
 struct StepInfo {
@@ -232,10 +131,10 @@ __global__ void __maxnreg__(128)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int hkv = kSlotMajor ? blockIdx.y : blockIdx.x;
-  // CTA-pair mode: clusters of 2 along y; slot lists; shared pairs multicast Q/dO
+  const int hkv = blockIdx.y;
+  // CTA-pair mode: clusters of 2 along x (slots); slot lists; shared pairs multicast Q/dO
   const bool cluster_mode = p.pair_shared != nullptr;
-  const int slot = kSlotMajor ? blockIdx.x : blockIdx.y;
+  const int slot = blockIdx.x;
   const int kb = p.order ? p.order[slot] : slot;   // -1: padding slot (cluster mode)
   const int li = cluster_mode ? slot : kb;         // step-list index
   const uint32_t crank = cluster_mode ? cluster_ctarank() : 0;
@@ -264,13 +163,11 @@ __global__ void __maxnreg__(128)
       mbar_init(&sm.bar_full[i], 1);
       mbar_init(&sm.bar_empty[i], shared ? 2 : 1);  // shared: both CTAs' MMAs release a stage
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.bar_sdp_full[b], 1);
-      mbar_init(&sm.bar_p_ready[b], 256);
-      mbar_init(&sm.bar_mma_done[b], 1);
-      mbar_init(&sm.bar_dq_full[b], 1);
-      mbar_init(&sm.bar_dq_empty[b], 128);
-    }
+    mbar_init(&sm.bar_s_full, 1);
+    for (int j = 0; j < kBwdPChunks; ++j) mbar_init(&sm.bar_p_ready[j], 256);
+    mbar_init(&sm.bar_mma_done, 1);
+    mbar_init(&sm.bar_dq_full, 1);
+    mbar_init(&sm.bar_dq_empty, 128);
     mbar_init(&sm.bar_kvt, 256);
     mbar_init(&sm.bar_dp_full, 1);
     mbar_init(&sm.bar_ds_ready, 256);
@@ -339,16 +236,11 @@ __global__ void __maxnreg__(128)
       const uint32_t id_s = idesc_bf16(128, 64, 0, 0);    // S^T, dP^T: K-major x K-major
       const uint32_t id_kv = idesc_bf16(128, 128, 0, 1);  // dV, dK: (TMEM|K-major) x MN-major
       const uint32_t id_q = idesc_bf16(128, 64, 1, 1);    // dQ^T: MN-major x MN-major
-      const uint64_t dk_k = sdesc_sw128(smem_u32(sm.k), 16, 1024);            // K, K-major
-      const uint64_t dk_v = sdesc_sw128(smem_u32(sm.v), 16, 1024);            // V, K-major
       const uint64_t dk_kmn = sdesc_sw128(smem_u32(sm.k), kTileBytes / 2, 1024);  // K, MN-major
       const uint64_t d_q0 = sdesc_sw128(smem_u32(sm.st[0].q), 16, 1024);         // K-major
       const uint64_t d_q0mn = sdesc_sw128(smem_u32(sm.st[0].q), kHalfBytes / 2, 1024);
-      const uint64_t d_ds0 = sdesc_sw128(smem_u32(sm.ds[0]), 16, 1024);
+      const uint64_t d_ds0 = sdesc_sw128(smem_u32(sm.ds), 16, 1024);
       constexpr uint32_t kStage16 = sizeof(Stage) >> 4, kDo16 = kHalfBytes >> 4;
-      constexpr uint32_t kDs16 = kDsBytes >> 4;
-#if BAM_BWD_KVT
-      (void)dk_k; (void)dk_v; (void)kDs16;
       const uint32_t tK = tmem + kColK, tV = tmem + kColV, tS = tmem + kColS, tDP = tmem + kColDP;
       mbar_wait(&sm.bar_kvt, 0);  // K / V rows stored into TMEM by the compute warps
       // S^T(s) = K Q^T (A = K from TMEM) -> S; S(s) overwrites P^T(s-1), the A operand of
@@ -364,12 +256,12 @@ __global__ void __maxnreg__(128)
           const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
           mma_ts_w(tS, tK + 8 * kk, dq + kq, id_s, kk > 0, leader);
         }
-        tc_commit_w(&sm.bar_sdp_full[0], leader);
+        tc_commit_w(&sm.bar_s_full, leader);
       };
       // dP^T(s) = V dO^T (A = V from TMEM) -> dP, once dQ^T(s-1) has been drained from it
       auto issue_dp = [&](int s) {
         const int st = s % kStages;
-        if (s > 0) BAM_XWAIT(&sm.bar_dq_empty[0], (s - 1) & 1);
+        if (s > 0) mbar_wait(&sm.bar_dq_empty, (s - 1) & 1);
         BAM_TRACE_EV(trace_cta && leader, 1, s);
         tc_fence_after();
         const uint64_t ddo = d_q0 + st * kStage16 + kDo16;
@@ -387,15 +279,24 @@ __global__ void __maxnreg__(128)
         const int st = s % kStages;
         const uint32_t ph = s & 1;
         const uint64_t dqmn = d_q0mn + st * kStage16, ddomn = dqmn + kDo16;
-        BAM_XWAIT(&sm.bar_p_ready[0], ph);
-        BAM_TRACE_EV(trace_cta && leader, 2, s);
-        tc_fence_after();
+        // dV += P^T dO  (A = P^T bf16 in the S columns).  P^T(s) arrives in two chunks
+        // of 16 queries per warpgroup (bar_p_ready[j]): chunk j feeds the 16-query
+        // steps kk = j (warpgroup 0) and 2 + j (warpgroup 1), so half of dV(s) runs
+        // while the compute warps finish the other half of P
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO  (A = P^T bf16 in the S columns)
-          mma_ts_w(tmem + kColDV, tS + (kk >> 1) * 32 + (kk & 1) * 8, ddomn + kk * 128, id_kv,
-                   (s > 0 || kk > 0), leader);
+        for (int j = 0; j < kBwdPChunks; ++j) {
+          mbar_wait(&sm.bar_p_ready[j], ph);
+          BAM_TRACE_EV(trace_cta && leader, 2, s);
+          tc_fence_after();
+#pragma unroll
+          for (int u = 0; u < 4 / kBwdPChunks; ++u) {
+            const int kk = 2 * u + j;
+            mma_ts_w(tmem + kColDV, tS + (kk >> 1) * 32 + (kk & 1) * 8, ddomn + kk * 128, id_kv,
+                     (s > 0 || j > 0 || u > 0), leader);
+          }
+        }
         if (s + 1 < nsteps) issue_s(s + 1);  // overlaps the compute warps' dS(s)
-        BAM_XWAIT(&sm.bar_ds_ready, ph);
+        mbar_wait(&sm.bar_ds_ready, ph);
         BAM_TRACE_EV(trace_cta && leader, 14, s);
         tc_fence_after();
         // dQ^T first and committed on its own: the dQ warps drain it (and dP(s+1),
@@ -403,7 +304,7 @@ __global__ void __maxnreg__(128)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T -> the dP columns
           mma_ss_w(tDP, dk_kmn + kk * 128, d_ds0 + kk * 128, id_q, kk > 0, leader);
-        tc_commit_w(&sm.bar_dq_full[0], leader);
+        tc_commit_w(&sm.bar_dq_full, leader);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q  (A = dS^T K-major in shared memory)
           mma_ss_w(tmem + kColDK, d_ds0 + 2 * kk, dqmn + kk * 128, id_kv, (s > 0 || kk > 0),
@@ -415,75 +316,7 @@ __global__ void __maxnreg__(128)
         BAM_TRACE_EV(trace_cta && leader, 3, s);
         if (s + 1 < nsteps) issue_dp(s + 1);
       }
-      tc_commit_w(&sm.bar_mma_done[0], leader);
-#else
-      auto issue_sdp = [&](int s) {
-        const int st = s % kStages, b = s & 1;
-        mbar_wait(&sm.bar_full[st], (s / kStages) & 1);
-        BAM_TRACE_EV(trace_cta && leader, 11, s);
-        // S_b still holds P^T(s-2), read by dV(s-2): issued earlier by this warp, and
-        // tcgen05.mma ops from one thread execute in issue order, so no wait is needed.
-        tc_fence_after();
-        BAM_TRACE_EV(trace_cta && leader, 16, s);
-        const uint32_t tS = tmem + kColBuf + 128 * b, tdP = tS + 64;
-        const uint64_t dq = d_q0 + st * kStage16, ddo = dq + kDo16;
-        BAM_TRACE_EV(trace_cta && leader, 0, s);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t ka = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
-          const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
-          mma_ss_w(tS, dk_k + ka, dq + kq, id_s, kk > 0, leader);
-        }
-        BAM_TRACE_EV(trace_cta && leader, 12, s);
-        if (s >= 2) BAM_XWAIT(&sm.bar_dq_empty[b], ((s >> 1) - 1) & 1);  // dQ^T(s-2) drained
-        BAM_TRACE_EV(trace_cta && leader, 1, s);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t ka = ((kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32) >> 4;
-          const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
-          mma_ss_w(tdP, dk_v + ka, ddo + kq, id_s, kk > 0, leader);
-        }
-        tc_commit_w(&sm.bar_sdp_full[b], leader);
-        BAM_TRACE_EV(trace_cta && leader, 13, s);
-      };
-      mbar_wait(&sm.bar_kv, 0);
-      issue_sdp(0);
-      for (int s = 0; s < nsteps; ++s) {
-        const int st = s % kStages, b = s & 1;
-        if (s + 1 < nsteps) issue_sdp(s + 1);
-        const uint64_t dqmn = d_q0mn + st * kStage16, ddomn = dqmn + kDo16;
-        const uint64_t dds = d_ds0 + b * kDs16;
-        const uint32_t tS = tmem + kColBuf + 128 * b, tDQ = tS + 64;
-        BAM_XWAIT(&sm.bar_p_ready[b], (s >> 1) & 1);
-        BAM_TRACE_EV(trace_cta && leader, 2, s);
-        tc_fence_after();
-        // dV += P^T dO   (K = 64 queries: 4 steps of 16 rows = 2048 B)
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // P^T for queries [16kk, 16kk+16) at TMEM col 32(kk>>1)+8(kk&1)
-          mma_ts_w(tmem + kColDV, tS + (kk >> 1) * 32 + (kk & 1) * 8, ddomn + kk * 128, id_kv,
-                   (s > 0 || kk > 0), leader);
-        BAM_TRACE_EV(trace_cta && leader, 14, s);
-        // dK += dS^T Q   (A = dS^T from TMEM, like P^T but 16 columns further)
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ts_w(tmem + kColDK, tS + (kk >> 1) * 32 + 16 + (kk & 1) * 8, dqmn + kk * 128, id_kv,
-                   (s > 0 || kk > 0), leader);
-        BAM_TRACE_EV(trace_cta && leader, 15, s);
-        // dQ^T = K^T dS^T  (K = 128 keys: 8 steps of 16 key rows = 2048 B); dS^T as MN-major
-        // B uses the same start address with LBO unused (N = 64 = one swizzle atom)
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ss_w(tDQ, dk_kmn + kk * 128, dds + kk * 128, id_q, kk > 0, leader);
-        tc_commit_w(&sm.bar_dq_full[b], leader);
-        if (shared)
-          tc_commit_mc_w(&sm.bar_empty[st], 0x3, leader);  // the stage is filled by both CTAs
-        else
-          tc_commit_w(&sm.bar_empty[st], leader);
-        tc_commit_w(&sm.bar_mma_done[b], leader);
-        BAM_TRACE_EV(trace_cta && leader, 3, s);
-      }
-#endif
+      tc_commit_w(&sm.bar_mma_done, leader);
     }
   } else if (warp < kWarpDQ) {
     // ------------------------------------------------------------ compute warps 0-7
@@ -496,7 +329,6 @@ __global__ void __maxnreg__(128)
     const long long dk = p.desc[kg];
     const float scale_log2 = p.scale * 1.4426950408889634f;
     StepIter it(col, grp, hkv, p.h_begin);
-#if BAM_BWD_KVT
     if (nsteps > 0) {
       // Row r of K (warpgroup 0) / V (warpgroup 1) from the swizzled tile into
       // TMEM lane r as bf16 pairs: column j = head-dim elements 2j, 2j+1.
@@ -520,14 +352,14 @@ __global__ void __maxnreg__(128)
       tc_fence_before();
       mbar_arrive(&sm.bar_kvt);
     }
-    for (int s = 0; s < (kMmaOnly ? 0 : nsteps); ++s) {
+    for (int s = 0; s < nsteps; ++s) {
       const int st = s % kStages;
       const uint32_t ph = s & 1;
       const StepInfo si = it.get();
       it.next();
       const uint32_t tS = tmem + kColS + lane_base, tdP = tmem + kColDP + lane_base;
-      const uint32_t ds_row = smem_u32(sm.ds[0]) + r * 128;
-      mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_sdp_full[0], ph);
+      const uint32_t ds_row = smem_u32(sm.ds) + r * 128;
+      mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_s_full, ph);
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 4, s);
       tc_fence_after();
       uint32_t sr[32];
@@ -542,24 +374,31 @@ __global__ void __maxnreg__(128)
       }
       tmem_wait_ld();
       // this warpgroup's 32 queries: lse*log2e at ld[32c ..], D at ld[64 + 32c ..]
-      const float4* lse4 = reinterpret_cast<const float4*>(sm.ld[st] + c * 32);
-      const float4* d4 = reinterpret_cast<const float4*>(sm.ld[st] + 64 + c * 32);
-      {
-        uint32_t pk[16];
+      // (broadcast loads: every lane reads the same 16-B pairs)
+      const float* lse_s = sm.ld[st] + c * 32;
+      const float* d_s = sm.ld[st] + 64 + c * 32;
+      // P^T over this warpgroup's own S columns, released in kBwdPChunks chunks
 #pragma unroll
-        for (int i2 = 0; i2 < 16; ++i2) {
-          const float4 l4 = lse4[i2 >> 1];
-          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], (i2 & 1) ? l4.z : l4.x,
-                                   (i2 & 1) ? l4.w : l4.y, scale_log2, i2, allow);
+      for (int j = 0; j < kBwdPChunks; ++j) {
+        constexpr int kPer = 16 / kBwdPChunks;
+        uint32_t pk[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int i2 = j * kPer + u;
+          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], lse_s[2 * i2],
+                                   lse_s[2 * i2 + 1], scale_log2, i2, allow);
           sr[2 * i2] = __float_as_uint(pp.x);
           sr[2 * i2 + 1] = __float_as_uint(pp.y);
-          pk[i2] = pack_bf16(pp.x, pp.y);
+          pk[u] = pack_bf16(pp.x, pp.y);
         }
-        BAM_TMEM_ST16(tS + c * 32, pk);  // P^T over this warpgroup's own S columns
+        if constexpr (kPer == 16)
+          BAM_TMEM_ST16(tS + c * 32, pk);
+        else
+          BAM_TMEM_ST8(tS + c * 32 + j * 8, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm.bar_p_ready[j]);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&sm.bar_p_ready[0]);
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 5, s);
       mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_dp_full, ph);
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 6, s);
@@ -570,11 +409,10 @@ __global__ void __maxnreg__(128)
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 16, s);
 #pragma unroll
       for (int i2 = 0; i2 < 16; ++i2) {
-        const float4 D4 = d4[i2 >> 1];
         const float2 ds = ds_pair(make_float2(__uint_as_float(sr[2 * i2]),
                                               __uint_as_float(sr[2 * i2 + 1])),
-                                  dr[2 * i2], dr[2 * i2 + 1], (i2 & 1) ? D4.z : D4.x,
-                                  (i2 & 1) ? D4.w : D4.y);
+                                  dr[2 * i2], dr[2 * i2 + 1], d_s[2 * i2],
+                                  d_s[2 * i2 + 1]);
         dsk[i2] = pack_bf16(ds.x, ds.y);
       }
       // dS^T row r, query columns 32c .. 32c+31 (the A operand of dK, B of dQ^T)
@@ -593,68 +431,6 @@ __global__ void __maxnreg__(128)
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 7, s);
       mbar_arrive(&sm.bar_ds_ready);
     }
-#else
-    for (int s = 0; s < (kMmaOnly ? 0 : nsteps); ++s) {
-      const int st = s % kStages, b = s & 1;
-      const StepInfo si = it.get();
-      it.next();
-      const uint32_t tS = tmem + kColBuf + 128 * b + lane_base, tdP = tS + 64;
-      const uint32_t ds_row = smem_u32(sm.ds[b]) + r * 128;
-      mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_sdp_full[b], (s >> 1) & 1);
-      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 4, s);
-      BAM_TRACE_EV(trace_cta && threadIdx.x == 128, 6, s);
-      tc_fence_after();
-      uint32_t sr[32], dr[32];
-      BAM_TMEM_LD32(tS + c * 32, sr);
-      BAM_TMEM_LD32(tdP + c * 32, dr);
-      uint32_t allow = si.cls ? 0xFFFFFFFFu : 0u;  // class 0: a pair step this key block skips
-      if (si.cls == 2) {  // PARTIAL tile: descriptor predicate for these 32 queries
-        const long long qg0 = (long long)p.q_gid[si.jq] * 128 + si.half * 64 + c * 32;
-        allow = 0;
-#pragma unroll 1
-        for (int i = 0; i < 32; ++i)
-          allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
-      }
-      tmem_wait_ld();
-      BAM_TRACE_EV(threadIdx.x == 0, 17, s);
-      const float4* lse4 = reinterpret_cast<const float4*>(sm.ld[st] + c * 32);
-      const float4* d4 = reinterpret_cast<const float4*>(sm.ld[st] + 64 + c * 32);
-      uint32_t pk[16], dsk[16];
-#pragma unroll
-      for (int i2 = 0; i2 < 16; ++i2) {
-        const float4 l4 = lse4[i2 >> 1], D4 = d4[i2 >> 1];
-        const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], (i2 & 1) ? l4.z : l4.x,
-                                 (i2 & 1) ? l4.w : l4.y, scale_log2, i2, allow);
-        const float2 ds = ds_pair(pp, dr[2 * i2], dr[2 * i2 + 1], (i2 & 1) ? D4.z : D4.x,
-                                  (i2 & 1) ? D4.w : D4.y);
-        pk[i2] = pack_bf16(pp.x, pp.y);
-        dsk[i2] = pack_bf16(ds.x, ds.y);
-      }
-      BAM_TRACE_EV(threadIdx.x == 0, 18, s);
-      // P^T (bf16 pairs) goes over the S columns this warpgroup itself read,
-      // [32c, 32c+16): the other warpgroup may still be loading its own columns.
-      BAM_TMEM_ST16(tS + c * 32, pk);
-      // dS^T (bf16) too: over [32c+16, 32c+32) as the TMEM A operand of dK, and
-      // into shared memory as the B operand of dQ^T
-      BAM_TMEM_ST16(tS + c * 32 + 16, dsk);
-      // dS^T row r, query columns 32c .. 32c+31: four 16-B chunks, 128-B swizzle
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const uint32_t chunk = (uint32_t)(c * 4 + q4) ^ (uint32_t)(r & 7);
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ds_row + chunk * 16),
-                     "r"(dsk[q4 * 4]), "r"(dsk[q4 * 4 + 1]), "r"(dsk[q4 * 4 + 2]),
-                     "r"(dsk[q4 * 4 + 3])
-                     : "memory");
-      }
-      tmem_wait_st();
-      BAM_TRACE_EV(threadIdx.x == 0, 19, s);
-      fence_async_smem();
-      tc_fence_before();
-      BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 5, s);
-      BAM_TRACE_EV(trace_cta && threadIdx.x == 128, 7, s);
-      mbar_arrive(&sm.bar_p_ready[b]);
-    }
-#endif
     // epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled), fp32 rows
     if (kb < 0) goto done;  // padding slot of the last cluster
     {
@@ -666,19 +442,13 @@ __global__ void __maxnreg__(128)
       dst = p.dkv_peers[owner] +
             (((int64_t)(c == 0 ? 1 : 0) * p.Hkv + hkv) * p.dkv_rows_per_owner + lr) * 128;
     } else {
-      dst = (c == 0 ? p.dv : p.dk) +
-            (p.dkv_head_major ? ((int64_t)hkv * p.k_rows * 128 + row) * 128
-                              : (row * p.Hkv + hkv) * 128);
+      dst = (c == 0 ? p.dv : p.dk) + (row * p.Hkv + hkv) * 128;
     }
     const float mul = c == 0 ? 1.f : p.scale;
     if (nsteps > 0) {
-#if BAM_BWD_KVT
-      mbar_wait_sleep(&sm.bar_mma_done[0], 0);
-#else
-      mbar_wait_sleep(&sm.bar_mma_done[(nsteps - 1) & 1], ((nsteps - 1) >> 1) & 1);
-#endif
+      mbar_wait_sleep(&sm.bar_mma_done, 0);
       tc_fence_after();
-      if (BAM_EPI_BULK_LOCAL || p.dkv_peers != nullptr) {
+      if (p.dkv_peers != nullptr) {
         // fused reduce-scatter: rows staged in the (now idle) Q/dO stages, 272-B
         // pitch (conflict-free 16-B stores), then one 256-B bulk copy per half
         // row; the CTA waits only for the shared-memory reads, not for the
@@ -738,27 +508,15 @@ __global__ void __maxnreg__(128)
     const int d = (warp - kWarpDQ) * 32 + lane;
     const uint32_t lane_base = ((warp - kWarpDQ) * 32) << 16;
     StepIter it(col, grp, hkv, p.h_begin);
-#if BAM_DQ_BULK
-#if BAM_BWD_KVT
     float* const dq_stage0 = reinterpret_cast<float*>(sm.v);  // V lives in TMEM by now
-#else
-    float* const dq_stage0 = sm.dq_stage;
-#endif
     int n_export = 0;
-#endif
-    for (int s = 0; s < (kMmaOnly ? 0 : nsteps); ++s) {
-#if BAM_BWD_KVT
-      const int b = 0;
-      const uint32_t tDQ = tmem + kColDP, dq_par = s & 1;
-#else
-      const int b = s & 1;
-      const uint32_t tDQ = tmem + kColBuf + 128 * b + 64, dq_par = (s >> 1) & 1;
-#endif
+    for (int s = 0; s < nsteps; ++s) {
+      const uint32_t tDQ = tmem + kColDP;
       const StepInfo si = it.get();
       it.next();
       float* dst = p.dq_acc + ((int64_t)si.h * Tq + si.jq * 128 + si.half * 64) * 128 + d;
       // on the K/V-in-TMEM chain (dP(s+1) waits for this drain): short back-off
-      mbar_wait_sleep<BAM_DQ_SLEEP_NS>(&sm.bar_dq_full[b], dq_par);
+      mbar_wait_sleep<BAM_DQ_SLEEP_NS>(&sm.bar_dq_full, s & 1);
       BAM_TRACE_EV(trace_cta && threadIdx.x == kWarpDQ * 32, 8, s);
       tc_fence_after();
       uint32_t a[32], c2[32];
@@ -766,23 +524,12 @@ __global__ void __maxnreg__(128)
       BAM_TMEM_LD32(tDQ + lane_base + 32, c2);
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&sm.bar_dq_empty[b]);
-#ifdef BAM_EXPERIMENT_NO_DQ_RED
-      if (a[0] == 0x7fc00001u) red_add(dst, 1.f);   // keep the loads live, skip the reductions
-      continue;
-#endif
+      mbar_arrive(&sm.bar_dq_empty);
       if (si.cls == 0) continue;  // pair step this key block skips: dQ^T is zero
-#if BAM_DQ_BULK
       // staging buffer free once the bulk reduce that last used it has read it
       const bool dq_leader = threadIdx.x == kWarpDQ * 32;
-#if BAM_BWD_KVT && BAM_DQ_STAGE2
       float* const dq_stage = (n_export++ & 1) ? sm.dq_stage : dq_stage0;
       if (dq_leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-#else
-      float* const dq_stage = dq_stage0;
-      (void)n_export;
-      if (dq_leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-#endif
       BAM_TRACE_EV(trace_cta && dq_leader, 13, s);
       named_bar_sync(1, 128);
 #pragma unroll
@@ -800,25 +547,12 @@ __global__ void __maxnreg__(128)
             "r"(smem_u32(dq_stage)), "n"(64 * 128 * 4)
             : "memory");
       }
-#elif BAM_DQ_MODE == 2
-      red_add_quads(dst - d, d, a, 0);
-      red_add_quads(dst - d, d, c2, 32);
-#else
-      red_add_rows<0>(dst, a);
-      red_add_rows<32>(dst, c2);
-#endif
       BAM_TRACE_EV(trace_cta && threadIdx.x == kWarpDQ * 32, 9, s);
     }
-#if BAM_DQ_BULK
     if (threadIdx.x == kWarpDQ * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-#endif
   }
   tc_fence_before();
   __syncthreads();
-  if (p.head_done != nullptr && threadIdx.x == 0) {  // this CTA's dK/dV rows are written
-    __threadfence();
-    atomicAdd(p.head_done + hkv, 1);
-  }
   if (cluster_mode) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == kWarpMMA) {
     tc_fence_after();
@@ -1008,20 +742,20 @@ int bam_attn_bwd_main(const BamAttnBwdParams* pp, void* stream) {
     BAM_CHECK_ARG(p.n_slots >= 2 && p.n_slots % 2 == 0 && p.order != nullptr,
                   "bam_attn_bwd: pair mode needs an even n_slots=%d and slot_kb", p.n_slots);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = bwd::kSlotMajor ? dim3(p.n_slots, p.Hkv) : dim3(p.Hkv, p.n_slots);
+    cfg.gridDim = dim3(p.n_slots, p.Hkv);
     cfg.blockDim = dim3(bwd::kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = bwd::kSlotMajor ? 2 : 1;
-    attr[0].val.clusterDim.y = bwd::kSlotMajor ? 1 : 2;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     BAM_CUDA_TRY(cudaLaunchKernelEx(&cfg, bwd::attn_bwd_kernel, mq, mk, mv, mdo, p));
   } else {
-    const dim3 grid = bwd::kSlotMajor ? dim3(p.nb, p.Hkv) : dim3(p.Hkv, p.nb);
+    const dim3 grid(p.nb, p.Hkv);
     bwd::attn_bwd_kernel<<<grid, bwd::kThreads, smem, (cudaStream_t)stream>>>(mq, mk, mv, mdo, p);
   }
   BAM_LAUNCH_CHECK();

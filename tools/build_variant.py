@@ -2,7 +2,7 @@
 """Build an A/B variant of libbam.so: one source recompiled with extra -D
 flags, linked with the default objects of the others.
 
-  python tools/build_variant.py attn_bwd.cu libbam_x.so -DBAM_BWD_KVT=0
+  python tools/build_variant.py attn_fwd.cu libbam_x.so -DBAM_FWD_P_CHUNKS=4
 
 The variant is selected at run time with BAM_LIB_PATH=<path>.
 """
