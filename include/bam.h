@@ -271,15 +271,14 @@ int bam_attn_fwd_qpairs(const BamAttnFwdParams* p, const int32_t* pair_ids, int3
  * Builds, on `stream`, everything the attention kernels need for one rank of a
  * CP plan from the tile classes and the block assignment: the rank-major
  * gathered layout (k_row; this rank's blocks q_gid ascending), the CSR rows
- * (fwd; `row_tiles` with this rank's key blocks first when world > 1,
- * `row_tiles_asc` ascending -- the same buffer when world == 1) and CSC
- * columns (bwd), the heavy-first orders, the backward CTA-pair step lists, the
+ * (fwd; this rank's key blocks first when world > 1, each group ascending)
+ * and CSC columns (bwd), the heavy-first orders, the backward CTA-pair step lists, the
  * forward query-block pairs and the whole-row items of the other blocks
  * (counts[0] shared pairs in fwd_pair_ids, counts[1] items in fwd_rest_items,
  * both on the device; see BamAttnFwdParams.dev_counts).
  * Sizes (int32 elements), with n_tiles = sum of W over this rank's blocks (its
  * LPT load) and P = ceil(nb/2), F = ceil(nq/2): k_row nb, q_gid nq, row_cnt nq,
- * row_off nq+1, row_tiles / row_tiles_asc / col_tiles n_tiles, col_cnt nb,
+ * row_off nq+1, row_tiles / col_tiles n_tiles, col_cnt nb,
  * col_off nb+1, fwd_order nq, bwd_order nb, slot_kb / slot_cnt 2P, slot_off
  * 2P+1, slot_tiles 2*n_tiles, pair_shared P, fwd_slot_q / fwd_slot_cnt 2F,
  * fwd_slot_off 2F+1, fwd_slot_tiles 2*n_tiles, fwd_shared F, fwd_pair_ids F,
@@ -290,7 +289,7 @@ typedef struct BamPlan {
   int32_t nb, nq, world, rank;
   int32_t max_blocks;       /* the largest per-rank block count (gathered rank stride) */
   int32_t pad_;
-  int32_t *k_row, *q_gid, *row_cnt, *row_off, *row_tiles, *row_tiles_asc;
+  int32_t *k_row, *q_gid, *row_cnt, *row_off, *row_tiles;
   int32_t *col_cnt, *col_off, *col_tiles, *fwd_order, *bwd_order;
   int32_t *slot_kb, *slot_cnt, *slot_off, *slot_tiles, *pair_shared;
   int32_t *fwd_slot_q, *fwd_slot_cnt, *fwd_slot_off, *fwd_slot_tiles, *fwd_shared;

@@ -35,7 +35,7 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("kv_rows_per_rank", c_i32), ("kv_head_major", c_i32), ("dev_counts", c_vp)]
 
 
-PLAN_BUFFERS = ("k_row", "q_gid", "row_cnt", "row_off", "row_tiles", "row_tiles_asc", "col_cnt",
+PLAN_BUFFERS = ("k_row", "q_gid", "row_cnt", "row_off", "row_tiles", "col_cnt",
                 "col_off", "col_tiles", "fwd_order", "bwd_order", "slot_kb", "slot_cnt",
                 "slot_off", "slot_tiles", "pair_shared", "fwd_slot_q", "fwd_slot_cnt",
                 "fwd_slot_off", "fwd_slot_tiles", "fwd_shared", "fwd_pair_ids",

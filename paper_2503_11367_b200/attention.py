@@ -75,7 +75,7 @@ def _plan_sizes(nb: int, nq: int, n_tiles: int) -> dict:
     """int32 element counts of bam_plan_build's buffers (include/bam.h)."""
     P, F, t = (nb + 1) // 2, (nq + 1) // 2, max(n_tiles, 1)
     return {"k_row": nb, "q_gid": nq, "row_cnt": nq, "row_off": nq + 1, "row_tiles": t,
-            "row_tiles_asc": t, "col_cnt": nb, "col_off": nb + 1, "col_tiles": t,
+            "col_cnt": nb, "col_off": nb + 1, "col_tiles": t,
             "fwd_order": nq, "bwd_order": nb, "slot_kb": 2 * P, "slot_cnt": 2 * P,
             "slot_off": 2 * P + 1, "slot_tiles": 2 * t, "pair_shared": P, "fwd_slot_q": 2 * F,
             "fwd_slot_cnt": 2 * F, "fwd_slot_off": 2 * F + 1, "fwd_slot_tiles": 2 * t,
@@ -93,8 +93,6 @@ def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, n
     nb = classes.shape[0]
     max_blocks = nq if max_blocks is None else max_blocks
     sizes = _plan_sizes(nb, nq, n_tiles)
-    if world == 1:
-        sizes.pop("row_tiles_asc")            # one buffer: the rows are ascending either way
     pad = lambda n: -(-n // 64) * 64            # noqa: E731  256-B aligned views (int4 items)
     ws = torch.empty(sum(pad(n) for n in sizes.values()), dtype=torch.int32,
                      device=classes.device)
@@ -102,8 +100,6 @@ def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, n
     for name, n in sizes.items():
         views[name] = ws[off:off + n]
         off += pad(n)
-    if world == 1:
-        views["row_tiles_asc"] = views["row_tiles"]
     bp = _lib.BamPlan(classes.data_ptr(), owner.data_ptr() if owner is not None else None, nb,
                       nq, world, rank, max_blocks, 0,
                       *[views[name].data_ptr() for name in _lib.PLAN_BUFFERS])

@@ -6,7 +6,7 @@
 //                        q_gid[nq] (this rank's blocks, ascending)
 //   list_* kernels       CSR rows (fwd) / CSC columns (bwd) of non-skip tiles
 //   sort_smem_kernel     heavy-first processing orders (-count, index)
-//   pair_lists_kernel    CTA-pair step lists (bwd) / query-block pairs (fwd)
+//   pair_lists_dense_kernel  CTA-pair step lists (bwd) / query-block pairs (fwd)
 //   fwd_pairs_kernel     compaction of the shared forward pairs and the
 //                        whole-row items of the others, with device counts
 //                        that the forward kernels read (grid = upper bound)
@@ -115,6 +115,103 @@ __global__ void __launch_bounds__(1024) fwd_pairs_kernel(const int32_t* __restri
   }
 }
 
+// CTA-pair step lists straight from the dense class matrix: one CTA per pair
+// of lists (a, b) = (order[2 pr], order[2 pr + 1]); the same lists as
+// bam_build_pair_lists' merge of the CSR/CSC arrays (tests compare them), but
+// every element is tested in parallel instead of one thread walking two sorted
+// lists.  kCols: lists are key-block columns over this rank's query blocks
+// (element e -> classes[q_gid[e]][list]); else query-block rows over the key
+// blocks (classes[q_gid[list]][e]).  Pass 1 (tiles == nullptr) counts: a pair
+// is shared when its union is at most 9/8 of the longer list; pass 2 fills.
+template <bool kCols>
+__global__ void __launch_bounds__(256) pair_lists_dense_kernel(
+    const uint8_t* __restrict__ classes, int32_t nb, const int32_t* __restrict__ q_gid,
+    int32_t n_elem, const int32_t* __restrict__ order, int32_t n_lists,
+    int32_t* __restrict__ slot_kb, int32_t* __restrict__ slot_cnt,
+    const int32_t* __restrict__ slot_off, int32_t* __restrict__ tiles,
+    int32_t* __restrict__ pair_shared) {
+  __shared__ int wa[8], wb[8], wu[8];
+  __shared__ int carry_a, carry_b;
+  const int pr = blockIdx.x;
+  const int a = order[2 * pr], b = 2 * pr + 1 < n_lists ? order[2 * pr + 1] : -1;
+  const uint8_t* ra = kCols ? classes + a : classes + (int64_t)q_gid[a] * nb;
+  const uint8_t* rb = b < 0 ? nullptr : (kCols ? classes + b : classes + (int64_t)q_gid[b] * nb);
+  const int w = threadIdx.x >> 5;
+  auto cls = [&](const uint8_t* base, int e) -> int {
+    if (base == nullptr || e >= n_elem) return 0;
+    return kCols ? base[(int64_t)q_gid[e] * nb] : base[e];
+  };
+  if (tiles == nullptr) {
+    int na = 0, nbb = 0, nu = 0;
+    for (int e = threadIdx.x; e < n_elem; e += 256) {
+      const int ca = cls(ra, e), cb = cls(rb, e);
+      na += ca != 0;
+      nbb += cb != 0;
+      nu += (ca | cb) != 0;
+    }
+    for (int o = 16; o; o >>= 1) {
+      na += __shfl_xor_sync(0xffffffffu, na, o);
+      nbb += __shfl_xor_sync(0xffffffffu, nbb, o);
+      nu += __shfl_xor_sync(0xffffffffu, nu, o);
+    }
+    if (lane_id() == 0) {
+      wa[w] = na;
+      wb[w] = nbb;
+      wu[w] = nu;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      na = nbb = nu = 0;
+      for (int i = 0; i < 8; ++i) {
+        na += wa[i];
+        nbb += wb[i];
+        nu += wu[i];
+      }
+      const int mx = na > nbb ? na : nbb;
+      const bool sh = b >= 0 && mx > 0 && 8 * nu <= 9 * mx;
+      pair_shared[pr] = sh;
+      slot_kb[2 * pr] = a;
+      slot_kb[2 * pr + 1] = b;
+      slot_cnt[2 * pr] = sh ? nu : na;
+      slot_cnt[2 * pr + 1] = sh ? nu : nbb;
+    }
+    return;
+  }
+  const bool sh = pair_shared[pr] != 0;
+  int32_t* oa = tiles + slot_off[2 * pr];
+  int32_t* ob = tiles + slot_off[2 * pr + 1];
+  if (threadIdx.x == 0) carry_a = carry_b = 0;
+  __syncthreads();
+  for (int base = 0; base < n_elem; base += 256) {
+    const int e = base + threadIdx.x;
+    const int ca = cls(ra, e), cb = cls(rb, e);
+    // shared: both slots walk the union (class 0 where a list lacks the element)
+    const bool ka = sh ? (ca | cb) != 0 : ca != 0, kb2 = sh ? ka : cb != 0;
+    const uint32_t ma = __ballot_sync(0xffffffffu, ka), mb = __ballot_sync(0xffffffffu, kb2);
+    if (lane_id() == 0) {
+      wa[w] = __popc(ma);
+      wb[w] = __popc(mb);
+    }
+    __syncthreads();
+    int pa = carry_a, pb = carry_b;
+    for (int i = 0; i < w; ++i) {
+      pa += wa[i];
+      pb += wb[i];
+    }
+    const uint32_t below = (1u << lane_id()) - 1;
+    if (ka) oa[pa + __popc(ma & below)] = (e << 2) | ca;
+    if (kb2) ob[pb + __popc(mb & below)] = (e << 2) | cb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 8; ++i) {
+        carry_a += wa[i];
+        carry_b += wb[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 static int64_t next_pow2(int64_t n) {
   int64_t p = 1;
   while (p < n) p <<= 1;
@@ -145,7 +242,7 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
                 "bam_plan_build: nb=%d nq=%d world=%d rank=%d max_blocks=%d", p.nb, p.nq, p.world,
                 p.rank, p.max_blocks);
   BAM_CHECK_ARG(p.world == 1 || p.owner, "bam_plan_build: world > 1 needs owner[]");
-  BAM_CHECK_ARG(p.k_row && p.q_gid && p.row_cnt && p.row_off && p.row_tiles && p.row_tiles_asc &&
+  BAM_CHECK_ARG(p.k_row && p.q_gid && p.row_cnt && p.row_off && p.row_tiles &&
                     p.col_cnt && p.col_off && p.col_tiles && p.fwd_order && p.bwd_order &&
                     p.slot_kb && p.slot_cnt && p.slot_off && p.slot_tiles && p.pair_shared &&
                     p.fwd_slot_q && p.fwd_slot_cnt && p.fwd_slot_off && p.fwd_slot_tiles &&
@@ -163,40 +260,33 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
   list_count_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.row_cnt, p.col_cnt);
   scan_kernel<<<1, 1024, 0, s>>>(p.row_cnt, nq, p.row_off);
   scan_kernel<<<1, 1024, 0, s>>>(p.col_cnt, nb, p.col_off);
-  list_fill_rows_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, p.row_off, p.row_tiles_asc,
-                                           nullptr, 0);
+  // rows: this rank's key blocks first under CP (the forward works on local K/V
+  // while the peers' rows are still arriving), each group ascending
+  list_fill_rows_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, p.row_off, p.row_tiles,
+                                           p.world > 1 ? p.owner : nullptr, p.rank);
   list_fill_cols_kernel<<<nb, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.col_off, p.col_tiles);
   BAM_LAUNCH_CHECK();
   // heavy-first orders (LPT's sort key: -count, then index)
   if (int rc = heavy_first(p.col_cnt, nb, p.bwd_order, s)) return rc;
   if (int rc = heavy_first(p.row_cnt, nq, p.fwd_order, s)) return rc;
-  // backward CTA-pair step lists over the columns
-  const int bp = (nb + 1) / 2;
-  bwd::pair_lists_kernel<<<(bp + 127) / 128, 128, 0, s>>>(p.col_off, p.col_tiles, p.bwd_order, nb,
-                                                          p.slot_kb, p.slot_cnt, nullptr, nullptr,
-                                                          p.pair_shared);
+  // backward CTA-pair step lists over the columns, forward query-block pairs over the rows
+  const int bp = (nb + 1) / 2, fp = (nq + 1) / 2;
+  pair_lists_dense_kernel<true><<<bp, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.bwd_order, nb,
+                                                   p.slot_kb, p.slot_cnt, nullptr, nullptr,
+                                                   p.pair_shared);
+  pair_lists_dense_kernel<false><<<fp, 256, 0, s>>>(p.classes, nb, p.q_gid, nb, p.fwd_order, nq,
+                                                    p.fwd_slot_q, p.fwd_slot_cnt, nullptr,
+                                                    nullptr, p.fwd_shared);
   scan_kernel<<<1, 1024, 0, s>>>(p.slot_cnt, 2 * bp, p.slot_off);
-  bwd::pair_lists_kernel<<<(bp + 127) / 128, 128, 0, s>>>(p.col_off, p.col_tiles, p.bwd_order, nb,
-                                                          p.slot_kb, p.slot_cnt, p.slot_off,
-                                                          p.slot_tiles, p.pair_shared);
-  // forward query-block pairs over the (ascending) rows
-  const int fp = (nq + 1) / 2;
-  bwd::pair_lists_kernel<<<(fp + 127) / 128, 128, 0, s>>>(p.row_off, p.row_tiles_asc, p.fwd_order,
-                                                          nq, p.fwd_slot_q, p.fwd_slot_cnt,
-                                                          nullptr, nullptr, p.fwd_shared);
   scan_kernel<<<1, 1024, 0, s>>>(p.fwd_slot_cnt, 2 * fp, p.fwd_slot_off);
-  bwd::pair_lists_kernel<<<(fp + 127) / 128, 128, 0, s>>>(p.row_off, p.row_tiles_asc, p.fwd_order,
-                                                          nq, p.fwd_slot_q, p.fwd_slot_cnt,
-                                                          p.fwd_slot_off, p.fwd_slot_tiles,
-                                                          p.fwd_shared);
+  pair_lists_dense_kernel<true><<<bp, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.bwd_order, nb,
+                                                   p.slot_kb, p.slot_cnt, p.slot_off,
+                                                   p.slot_tiles, p.pair_shared);
+  pair_lists_dense_kernel<false><<<fp, 256, 0, s>>>(p.classes, nb, p.q_gid, nb, p.fwd_order, nq,
+                                                    p.fwd_slot_q, p.fwd_slot_cnt, p.fwd_slot_off,
+                                                    p.fwd_slot_tiles, p.fwd_shared);
   fwd_pairs_kernel<<<1, 1024, 0, s>>>(p.fwd_shared, p.fwd_slot_q, p.row_cnt, fp, p.fwd_pair_ids,
                                       reinterpret_cast<int4*>(p.fwd_rest_items), p.counts);
   BAM_LAUNCH_CHECK();
-  // the kernels' rows: this rank's key blocks first (CP overlap)
-  if (p.row_tiles != p.row_tiles_asc) {
-    list_fill_rows_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, p.row_off, p.row_tiles,
-                                             p.world > 1 ? p.owner : nullptr, p.rank);
-    BAM_LAUNCH_CHECK();
-  }
   return kOk;
 }

@@ -433,6 +433,21 @@ def test_native_planner_matches_host_statement(policy, world):
             lb = {e >> 2 for e in asc[b]} if b >= 0 else set()
             mx = max(len(la), len(lb))
             fsh.append(b >= 0 and mx > 0 and 8 * len(la | lb) <= 9 * mx)
+        # the forward union lists against bam_build_pair_lists' merge of the ascending rows
+        rows_asc = torch.tensor([e for r in asc for e in r], dtype=torch.int32, device=dev)
+        fq = torch.empty(2 * fp, dtype=torch.int32, device=dev)
+        fcnt, foff = torch.empty_like(fq), torch.empty(2 * fp + 1, dtype=torch.int32, device=dev)
+        fsh_d = torch.empty(fp, dtype=torch.int32, device=dev)
+        _lib.call("bam_build_pair_lists", at.row_off.data_ptr(), rows_asc.data_ptr(),
+                  at.fwd_order.data_ptr(), nq, fq.data_ptr(), fcnt.data_ptr(), foff.data_ptr(),
+                  None, fsh_d.data_ptr())
+        ftiles = torch.empty(max(int(foff[-1]), 1), dtype=torch.int32, device=dev)
+        _lib.call("bam_build_pair_lists", at.row_off.data_ptr(), rows_asc.data_ptr(),
+                  at.fwd_order.data_ptr(), nq, fq.data_ptr(), fcnt.data_ptr(), foff.data_ptr(),
+                  ftiles.data_ptr(), fsh_d.data_ptr())
+        assert torch.equal(at.fwd_slot_q, fq) and torch.equal(at.fwd_slot_off, foff)
+        assert torch.equal(at.fwd_slot_tiles[:int(foff[-1])], ftiles[:int(foff[-1])])
+        assert fsh_d.cpu().tolist() == [int(x) for x in fsh]
         n_pairs, n_rest = at.counts.cpu().tolist()
         assert at.fwd_pair_ids[:n_pairs].cpu().tolist() == [pr for pr in range(fp) if fsh[pr]]
         rest = [j for pr in range(fp) if not fsh[pr] for j in fslot[pr].tolist() if j >= 0]

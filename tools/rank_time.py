@@ -12,6 +12,7 @@ kernel-only max/mean imbalance over the emulated ranks.
 import argparse
 import json
 import os
+import statistics
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -41,27 +42,35 @@ k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
 v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
 do = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
 nb = T // 128
-rows = []
+# every rank's plan and inputs first, then iterations round-robin over the ranks
+# (rank 0, 1, ..., world-1, 0, ...): run one after another, the later ranks would
+# see a hotter, more power-capped GPU and read slower
+ranks = []
 for r in range(args.world):
     plan = cp.make_cp_plan(desc, args.world, r, args.policy)
     lay = plan.layout
-    at = plan.attn
     k_all = torch.zeros((args.world * lay.max_blocks * 128, Hkv, 128), dtype=k.dtype, device=dev)
     v_all = torch.zeros_like(k_all)
     cp.permute_blocks([k, v], [k_all, v_all], lay.k_row[:nb], scatter=True)
     ql, dol = cp.shard_rows(q, do, layout=lay)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    f, b = [], []
-    for it in range(args.iters + 1):
+    ranks.append((plan, k_all, v_all, ql, dol))
+times = [([], []) for _ in range(args.world)]
+for it in range(args.iters + 1):
+    for r, (plan, k_all, v_all, ql, dol) in enumerate(ranks):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record()
-        o, lse = A.attn_forward(ql, k_all, v_all, at)
+        o, lse = A.attn_forward(ql, k_all, v_all, plan.attn)
         ev[1].record()
-        ws = A.BackwardWorkspace(ql, o, lse, dol, at, None)
+        ws = A.BackwardWorkspace(ql, o, lse, dol, plan.attn, None)
         ws.main(k_all, v_all, timer=(ev[2], ev[3]))
         torch.cuda.synchronize()
         if it:
-            f.append(ev[0].elapsed_time(ev[1]))
-            b.append(ev[2].elapsed_time(ev[3]))
+            times[r][0].append(ev[0].elapsed_time(ev[1]))
+            times[r][1].append(ev[2].elapsed_time(ev[3]))
+rows = []
+for r, (plan, k_all, v_all, ql, dol) in enumerate(ranks):
+    lay, at = plan.layout, plan.attn
+    f, b = statistics.median(times[r][0]), statistics.median(times[r][1])
     # cost features: tiles (the LPT load W), PARTIAL tiles, backward steps including the
     # class-0 padding of shared CTA-pair union lists, forward pair-union padding
     tiles = int(at.row_off[-1])
@@ -71,14 +80,15 @@ for r in range(args.world):
     fwd_union = int(sum(int(at.fwd_slot_off[2 * pr + 1] - at.fwd_slot_off[2 * pr])
                         for pr in at.fwd_pair_ids[:n_pairs].tolist())) if n_pairs else 0
     row = {"rank": r, "policy": args.policy, "n_local": lay.n_local,
-           "fwd_ms": round(min(f), 3), "bwd_main_ms": round(min(b), 3),
-           "kernel_ms": round(min(f) + min(b), 3), "tiles": tiles, "partial_tiles": partial,
+           "fwd_ms": round(f, 3), "bwd_main_ms": round(b, 3),
+           "kernel_ms": round(f + b, 3), "tiles": tiles, "partial_tiles": partial,
            "bwd_slot_steps": bwd_slots, "fwd_pair_union": fwd_union}
     rows.append(row)
     print(json.dumps(row), flush=True)
 ks = [x["kernel_ms"] for x in rows]
 ts = [x["tiles"] for x in rows]
 print(json.dumps({"config": args.config, "world": args.world, "policy": args.policy,
+                  "iters_round_robin": args.iters,
                   "imbalance_kernel": max(ks) / (sum(ks) / len(ks)),
                   "imbalance_fwd": max(x["fwd_ms"] for x in rows) /
                   (sum(x["fwd_ms"] for x in rows) / len(rows)),
