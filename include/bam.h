@@ -301,6 +301,11 @@ int bam_plan_build(const BamPlan* plan, void* stream);
  * after the stream's prior work, with a memory barrier): the arrival flags of
  * BamAttnFwdParams.kv_ready. */
 int bam_stream_write_i32(int32_t* dst, int32_t value, void* stream);
+/* Strided copy on the stream's copy engine (cudaMemcpy2DAsync, UVA
+ * direction, so a peer's buffer can be the source; no SM involved): height
+ * rows of width bytes, dst / src row pitches in bytes.  The CP K/V pulls. */
+int bam_copy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                int64_t height, void* stream);
 /* Stream-ordered wait (cuStreamWaitValue32, GEQ): the stream's later work
  * starts once *src >= value (no SM involved). */
 int bam_stream_wait_i32_geq(const int32_t* src, int32_t value, void* stream);

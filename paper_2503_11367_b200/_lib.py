@@ -90,6 +90,7 @@ SIGNATURES = {
                                          c_vp, c_vp, c_vp]),
     "bam_permute_blocks": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "bam_stream_write_i32": (c_i32, [c_vp, c_i32, c_vp]),
+    "bam_copy_2d": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
     "bam_stream_wait_i32_geq": (c_i32, [c_vp, c_i32, c_vp]),
     "bam_attn_fwd_2cta": (c_i32, [ctypes.POINTER(BamAttnFwdParams), c_vp, c_i32, c_vp, c_vp, c_vp,
                                   c_vp]),
@@ -161,6 +162,7 @@ KERNELS_PER_CALL = {
     "bam_reduce_partials_bf16": 1,
     "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1, "bam_plan_build": 15,
     "bam_stream_write_i32": 0, "bam_stream_wait_i32_geq": 0,   # stream memory operations
+    "bam_copy_2d": 0,                                         # copy engine
 }
 launch_count = 0
 

@@ -25,6 +25,7 @@ of group g overlaps the backward kernel of group g+1.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -185,6 +186,7 @@ class SymmExchange:
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
         self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
+        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "8"))
         self._cache = {}
 
     def _check(self, rows: int, kv0: int, nkv: int):
@@ -211,18 +213,23 @@ class SymmExchange:
         for ev in done:
             cur.wait_event(ev)
 
-    def gather_overlapped(self, rows: int, k_g: torch.Tensor, v_g: torch.Tensor):
+    def gather_overlapped(self, rows: int, k_g: torch.Tensor, v_g: torch.Tensor,
+                          head_chunks: int | None = None):
         """K/V all-gather that lets the attention start early, into HEAD-MAJOR
         buffers [nkv, world*rows, d]: this rank's rows go straight into the
         gathered buffers before the barrier (event ``ev_local``); the peers'
-        shards are pulled one KV head at a time (one contiguous chunk per
-        (peer, head)), each followed by a stream-ordered flag store
-        ``flags[peer*nkv + h] = epoch`` (bam_stream_write_i32, no SM) that the
-        forward kernel waits on per tile, so the first heads' tiles start
-        after 1/nkv of the transfer.  ``ev_all``: every pull landed.
+        shards are pulled in ``head_chunks`` groups of KV heads per peer (one
+        strided copy-engine copy per (peer, group, K|V), ``bam_copy_2d``), each
+        followed by stream-ordered flag stores ``flags[peer*nkv + h] = epoch``
+        (bam_stream_write_i32, no SM) that the forward kernel waits on per
+        tile, so the first heads' tiles start after a fraction of the transfer.
+        ``ev_all``: every pull landed.
         Returns (k_all, v_all, ev_local, ev_all, (flags, epoch))."""
         nkv, d = k_g.shape[1], self.d
         self._check(rows, 0, nkv)
+        chunks = max(1, min(nkv, head_chunks or self.head_chunks))
+        while nkv % chunks:
+            chunks -= 1
         n = k_g.shape[0]
         mine = self.kv[:2 * rows * nkv * d].view(2, nkv, rows, d)
         mine[0, :, :n].copy_(k_g.transpose(0, 1))
@@ -240,14 +247,21 @@ class SymmExchange:
             self.flags = torch.zeros(self.world * nkv, dtype=torch.int32, device=k_g.device)
         self.epoch += 1
         epoch = self.epoch
+        per = nkv // chunks
+        row_b = rows * d * 2                   # one head's rows of one rank, bytes
+        dpitch = self.world * row_b
 
         def pull(r):
             def fn():
                 src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, 0)
-                for h in range(nkv):
-                    k_all[h, r * rows:(r + 1) * rows].copy_(src[0, h])
-                    v_all[h, r * rows:(r + 1) * rows].copy_(src[1, h])
-                    _lib.call("bam_stream_write_i32", self.flags[r * nkv + h:].data_ptr(), epoch)
+                for g in range(chunks):
+                    h0 = g * per
+                    for t, dst in ((0, k_all), (1, v_all)):
+                        _lib.call("bam_copy_2d", dst[h0, r * rows:].data_ptr(), dpitch,
+                                  src[t, h0].data_ptr(), row_b, row_b, per)
+                    for h in range(h0, h0 + per):
+                        _lib.call("bam_stream_write_i32", self.flags[r * nkv + h:].data_ptr(),
+                                  epoch)
             return fn
         self._fan_out([pull((self.rank + step) % self.world) for step in range(1, self.world)])
         for t in (k_all, v_all):

@@ -189,6 +189,17 @@ extern "C" int bam_stream_write_i32(int32_t* dst, int32_t value, void* stream) {
   return bam::kOk;
 }
 
+// Strided copy on the stream's copy engine (cudaMemcpy2DAsync, UVA direction:
+// a peer's symmetric buffer works as the source): height rows of width bytes.
+extern "C" int bam_copy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                           int64_t width, int64_t height, void* stream) {
+  BAM_CHECK_ARG(dst && src && width > 0 && height > 0 && dpitch >= width && spitch >= width,
+                "bam_copy_2d: bad arguments");
+  BAM_CUDA_TRY(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width,
+                                 (size_t)height, cudaMemcpyDefault, (cudaStream_t)stream));
+  return bam::kOk;
+}
+
 extern "C" int bam_stream_wait_i32_geq(const int32_t* src, int32_t value, void* stream) {
   using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
   static Fn fn = nullptr;

@@ -51,8 +51,12 @@ rs_bytes = (world - 1) * rows * Hkv * D * 4 * 2              # fp32 dK and dV to
 steps = {
     ("kv_all_gather", "nccl"): (lambda: cp.gather_kv(k_loc, v_loc, lay), gather_bytes),
     ("kv_all_gather", "ce"): (lambda: ex.gather(rows, 0, k_loc, v_loc), gather_bytes),
-    ("kv_all_gather", "ce_head_major"): (lambda: ex.gather_overlapped(rows, k_loc, v_loc),
+    ("kv_all_gather", "ce_head_major"): (lambda: ex.gather_overlapped(rows, k_loc, v_loc, 8),
                                          gather_bytes),
+    ("kv_all_gather", "ce_head_major_2chunks"): (
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 2), gather_bytes),
+    ("kv_all_gather", "ce_head_major_1chunk"): (
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 1), gather_bytes),
     ("dkv_reduce_scatter", "nccl"): (lambda: cp.scatter_dkv(dk_all, dv_all, lay), rs_bytes),
     ("dkv_reduce_scatter", "ce"): (lambda: ex.reduce_scatter(rows, 0, dk_all, dv_all, n_loc),
                                    rs_bytes),
