@@ -448,7 +448,6 @@ __global__ void __maxnreg__(128)
       mbar_arrive(&sm.bar_kvt);
     }
     for (int s = 0; s < nsteps; ++s) {
-      const int st = s % kStages;
       const uint32_t ph = s & 1;
       const StepInfo si = it.get();
       it.next();
@@ -474,8 +473,8 @@ __global__ void __maxnreg__(128)
       constexpr float lse_s[32] = {}, d_s[32] = {};
 #else
       // (broadcast loads: every lane reads the same 16-B pairs)
-      const float* lse_s = sm.ld[st] + c * 32;
-      const float* d_s = sm.ld[st] + 64 + c * 32;
+      const float* lse_s = sm.ld[s % kStages] + c * 32;
+      const float* d_s = sm.ld[s % kStages] + 64 + c * 32;
 #endif
       // P^T over this warpgroup's own S columns, released in kBwdPChunks chunks
 #pragma unroll
