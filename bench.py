@@ -530,7 +530,7 @@ def main():
     peaks, peak_src = load_peaks()
     traffic = None
     try:   # DRAM bytes per launch from the committed ncu --set full capture (N=1 only)
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02", "traffic.json")) as fh:
             tr = json.load(fh).get(cfg["name"], {}).get("attn_bwd_kernel")
         if tr and world == tr["n_gpus"]:
             traffic = tr["dram_bytes_per_launch"]
@@ -585,7 +585,7 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "bam attn_bwd_kernel (tcgen05)",
                          "achieved": bwd_achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": bwd_achieved / peak, "traffic": traffic,
-                         "traffic_unit": "DRAM bytes per launch (ncu capture, profiles/r01)",
+                         "traffic_unit": "DRAM bytes per launch (the committed ncu --set full capture, profiles/r02/traffic.json)",
                          "peak_source": peak_src + " " + peak_kind +
                          " (kernel timed inside a long step)",
                          "peak_burst": peak_burst, "frac_of_burst": bwd_achieved / peak_burst,

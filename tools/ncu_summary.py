@@ -24,6 +24,12 @@ KEYS = [
     ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 red sectors (dQ reductions)"),
     ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2->SM bytes"),
     ("l1tex__m_l1tex2xbar_write_bytes.sum", "SM->L2 bytes"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory LSU wavefronts"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum", "shared-memory tensor-core wavefronts"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "shared-memory tensor-core wavefronts % of peak"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "shared-memory LSU wavefronts % of peak"),
     ("sm__icc_request_hit_rate.pct", "I-cache hit %"),
     ("launch__registers_per_thread", "registers / thread"),
     ("launch__shared_mem_per_block_dynamic", "dynamic smem / CTA"),
