@@ -87,8 +87,12 @@ for r, (plan, k_all, v_all, ql, dol) in enumerate(ranks):
     print(json.dumps(row), flush=True)
 ks = [x["kernel_ms"] for x in rows]
 ts = [x["tiles"] for x in rows]
+n_allowed = M.count_allowed(desc)
+flop = 14.0 * 128 * Hq * n_allowed
 print(json.dumps({"config": args.config, "world": args.world, "policy": args.policy,
                   "iters_round_robin": args.iters,
+                  "makespan_kernel_ms": max(ks),
+                  "tflops_emulated_whole_job": flop / max(ks) / 1e9,
                   "imbalance_kernel": max(ks) / (sum(ks) / len(ks)),
                   "imbalance_fwd": max(x["fwd_ms"] for x in rows) /
                   (sum(x["fwd_ms"] for x in rows) / len(rows)),
