@@ -10,6 +10,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -134,3 +135,54 @@ def test_cp_layout_unequal_counts():
     assert lay[2].local_blocks.tolist() == [5]
     # block b sits at owner*max + position among the owner's ascending blocks
     assert lay[0].k_row.tolist() == [0, 4, 5, 6, 1, 8, 7]
+
+
+def _transport_worker(rank, world, port, fail_ranks, result_dir):
+    """resolve_transport('auto') on a gloo group: the exchange 'fails' on the ranks
+    in fail_ranks; every rank must reach the same choice (a per-rank
+    fallback would leave ranks in mismatched collectives)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from types import SimpleNamespace
+
+    from paper_2503_11367_b200 import cp
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def exchange(hkv, d, device, group=None):
+            if rank in fail_ranks:
+                raise RuntimeError("no peer mapping on this rank")
+            return object()
+        plan = SimpleNamespace(layout=SimpleNamespace(world=world), exchange=exchange)
+        cp._TRANSPORT_CHOICE.clear()
+        choice = cp.resolve_transport("auto", plan, 8, 128, torch.device("cpu"))
+        with open(os.path.join(result_dir, f"choice{rank}"), "w") as fh:
+            fh.write(choice)
+        # forced transports and world 1 bypass the agreement
+        assert cp.resolve_transport("nccl", plan, 8, 128, torch.device("cpu")) == "nccl"
+        one = SimpleNamespace(layout=SimpleNamespace(world=1), exchange=exchange)
+        assert cp.resolve_transport("auto", one, 8, 128, torch.device("cpu")) == "local"
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_ranks,expected", [((), "ce"), ((1,), "nccl"), ((0, 2), "nccl")])
+def test_transport_choice_is_collective(tmp_path, fail_ranks, expected):
+    world = 3
+    mp.spawn(_transport_worker, args=(world, _free_port(), fail_ranks, str(tmp_path)),
+             nprocs=world, join=True)
+    choices = {open(os.path.join(tmp_path, f"choice{r}")).read() for r in range(world)}
+    assert choices == {expected}
+
+
+def test_exchange_capacity():
+    from paper_2503_11367_b200 import cp
+
+    # headroom of 1/8, rounded up to 1024 tokens, capped at the (rounded) sequence
+    assert cp.exchange_capacity(32896, 1024, 4) == 37888
+    assert cp.exchange_capacity(1024, 8, 1) == 1024
+    for rows, nb, world in ((128, 1024, 8), (16512, 1024, 8), (131072, 1024, 1)):
+        cap = cp.exchange_capacity(rows, nb, world)
+        assert cap >= rows and cap % 128 == 0

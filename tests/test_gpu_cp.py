@@ -454,3 +454,41 @@ def test_native_planner_matches_host_statement(policy, world):
         assert n_rest == len(rest)
         items = at.fwd_rest_items[:n_rest].cpu().tolist()
         assert items == [[j, 0, int(row_cnt[j]), -1] for j in rest]
+
+
+def test_copy_2d_and_kv_ready_validation():
+    """bam_copy_2d (the strided copy-engine copies of the CP K/V pulls) against
+    torch indexing; the C entry points reject kv_ready parameters the kernels
+    cannot honour (a 64-bit per-rank mask, a positive rank stride)."""
+    from paper_2503_11367_b200 import _lib
+    from paper_2503_11367_b200 import attention as A
+    from paper_2503_11367_b200 import cp
+    from paper_2503_11367_b200 import mask as M
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(2)
+    src = torch.randn(3, 5, 128, 128, device=dev, generator=g).to(torch.bfloat16)  # [2,nkv,rows,d]-like
+    dst = torch.zeros(5, 4 * 128, 128, dtype=torch.bfloat16, device=dev)
+    row_b = 128 * 128 * 2
+    _lib.call("bam_copy_2d", dst[1, 2 * 128:].data_ptr(), 4 * row_b, src[1, 1].data_ptr(), row_b,
+              row_b, 3)
+    torch.cuda.synchronize()
+    ref = torch.zeros_like(dst)
+    ref[1:4, 2 * 128:3 * 128] = src[1, 1:4]
+    assert torch.equal(dst, ref)
+    with pytest.raises(_lib.BamError):
+        _lib.call("bam_copy_2d", dst.data_ptr(), 16, src.data_ptr(), 32, 32, 1)   # pitch < width
+
+    mask = M.build_bitfield([("text", 512), ("img0", 512)])
+    plan = A.plan_for_mask(mask)
+    T = len(mask)
+    q = torch.randn(T, 4, 128, device=dev, generator=g).to(torch.bfloat16)
+    k = torch.randn(T, 2, 128, device=dev, generator=g).to(torch.bfloat16)
+    flags = torch.zeros(8, dtype=torch.int32, device=dev)
+    with pytest.raises(ValueError, match="kv_ready"):
+        A.attn_forward(q, k, k, plan, kv_ready=(flags, 1, 0, 0))
+    with pytest.raises(ValueError, match="kv_ready"):
+        A.attn_forward(q, k, k, plan, kv_ready=(flags, 1, 70, 1))
+    # a rank that owns no query block cannot run (more ranks than blocks)
+    with pytest.raises(ValueError, match="owns no query block"):
+        cp.make_cp_plan(mask, 16, 15, "zigzag")
