@@ -295,6 +295,7 @@ def cpu_planning_sample(segments, G, rows=16):
                       f"LPT over all {nb} blocks, G={G}",
             "reference_itself_measured_in_build_container": {
                 "config1_4K_block_workloads_s": 2.37, "config2_32K_block_workloads_s": 172.4,
+                "t2_extrapolated_128K_s": 172.4 * 16, "cores": 1,
                 "source": "tests/golden/config{1,2}_workloads.json reference_seconds "
                           "(make_golden.py ran the reference's block_workloads)"}}
 
