@@ -32,14 +32,15 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("items", c_vp), ("part_o", c_vp), ("part_ml", c_vp), ("n_items", c_i32),
                 ("pad_", c_i32), ("kv_ready", c_vp), ("kv_epoch", c_i32), ("kv_rank", c_i32),
-                ("kv_rows_per_rank", c_i32), ("kv_head_major", c_i32), ("dev_counts", c_vp)]
+                ("kv_rows_per_rank", c_i32), ("kv_head_major", c_i32), ("dev_counts", c_vp),
+                ("order_classes", c_vp)]
 
 
 PLAN_BUFFERS = ("k_row", "q_gid", "row_cnt", "row_off", "row_tiles", "col_cnt",
                 "col_off", "col_tiles", "fwd_order", "bwd_order", "slot_kb", "slot_cnt",
                 "slot_off", "slot_tiles", "pair_shared", "fwd_slot_q", "fwd_slot_cnt",
                 "fwd_slot_off", "fwd_slot_tiles", "fwd_shared", "fwd_pair_ids",
-                "fwd_rest_items", "counts")
+                "fwd_rest_items", "counts", "fwd_classes")
 
 
 class BamPlan(ctypes.Structure):
@@ -100,6 +101,7 @@ SIGNATURES = {
     "bam_selftest_umma": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bam_plan_build": (c_i32, [ctypes.POINTER(BamPlan), c_vp]),
     "bam_set_trace_buffer": (c_i32, [c_vp]),
+    "bam_set_cta_clock_buffer": (c_i32, [c_vp, c_vp]),
 }
 
 BAM_OK, BAM_INVALID_ARGUMENT, BAM_CUDA_ERROR, BAM_UNSUPPORTED, BAM_BUDGET_EXCEEDED = range(5)

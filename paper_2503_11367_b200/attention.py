@@ -63,6 +63,8 @@ class AttentionPlan:
     fwd_slot_tiles: torch.Tensor | None = None
     fwd_rest_items: torch.Tensor | None = None
     counts: torch.Tensor | None = None
+    # geometric work classes over fwd_order: the head-pair kernel's CTA order
+    fwd_classes: torch.Tensor | None = None
     row_cnt: torch.Tensor | None = None
     col_cnt: torch.Tensor | None = None
 
@@ -79,7 +81,8 @@ def _plan_sizes(nb: int, nq: int, n_tiles: int) -> dict:
             "fwd_order": nq, "bwd_order": nb, "slot_kb": 2 * P, "slot_cnt": 2 * P,
             "slot_off": 2 * P + 1, "slot_tiles": 2 * t, "pair_shared": P, "fwd_slot_q": 2 * F,
             "fwd_slot_cnt": 2 * F, "fwd_slot_off": 2 * F + 1, "fwd_slot_tiles": 2 * t,
-            "fwd_shared": F, "fwd_pair_ids": F, "fwd_rest_items": 4 * nq, "counts": 2}
+            "fwd_shared": F, "fwd_pair_ids": F, "fwd_rest_items": 4 * nq, "counts": 2,
+            "fwd_classes": 17}
 
 
 def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, nq: int,
@@ -113,7 +116,7 @@ def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, n
         fwd_pair_ids=views["fwd_pair_ids"], fwd_slot_q=views["fwd_slot_q"],
         fwd_slot_off=views["fwd_slot_off"], fwd_slot_tiles=views["fwd_slot_tiles"],
         fwd_rest_items=views["fwd_rest_items"].view(nq, 4), counts=views["counts"],
-        row_cnt=views["row_cnt"], col_cnt=views["col_cnt"])
+        fwd_classes=views["fwd_classes"], row_cnt=views["row_cnt"], col_cnt=views["col_cnt"])
 
 
 def build_plan(desc: torch.Tensor, classes: torch.Tensor | None = None,
@@ -270,6 +273,9 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
     p.kv_head_major = int(kv_head_major)
     if plan.counts is not None and schedule is None:
         p.dev_counts = plan.counts.data_ptr()
+    if (plan.fwd_classes is not None and schedule is None
+            and os.environ.get("BAM_FWD_CLASS_ORDER", "1") != "0"):
+        p.order_classes = plan.fwd_classes.data_ptr()
     if kv_ready is not None:
         # the head-pair, query-pair and one-head kernels honour the flags (not the
         # CTA-pair kernel, nor split-KV schedules)

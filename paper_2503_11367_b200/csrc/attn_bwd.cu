@@ -179,6 +179,7 @@ __global__ void __maxnreg__(128)
                     const BamAttnBwdParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  BAM_CTA_CLOCK_BEGIN();
   const uint32_t warp = warp_id(), lane = lane_id();
   const int hkv = blockIdx.y;
   // CTA-pair mode: clusters of 2 along x (slots); slot lists; shared pairs multicast Q/dO
@@ -657,6 +658,7 @@ __global__ void __maxnreg__(128)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  BAM_CTA_CLOCK_END(nsteps);
 }
 
 // ld[h, 0, row] = lse[h, row] * log2e, ld[h, 1, row] = sum_d dO[row, h, d] * O[row, h, d]
@@ -803,6 +805,20 @@ int bam_set_trace_buffer(void* buf) {
 #else
   (void)buf;
   set_last_error("libbam built without -DBAM_TRACE");
+  return BAM_UNSUPPORTED;
+#endif
+}
+
+// Development aid: install the per-CTA clock buffers ([CTAs][4] u64 of the
+// forward head-pair / backward kernels) of -DBAM_CTA_CLOCK builds.
+int bam_set_cta_clock_buffer(void* fwd_buf, void* bwd_buf) {
+#ifdef BAM_CTA_CLOCK
+  BAM_CUDA_TRY(cudaMemcpyToSymbol(g_bam_cta_clock, &bwd_buf, sizeof(bwd_buf)));
+  return fwd_set_cta_clock(fwd_buf);
+#else
+  (void)fwd_buf;
+  (void)bwd_buf;
+  set_last_error("libbam built without -DBAM_CTA_CLOCK");
   return BAM_UNSUPPORTED;
 #endif
 }

@@ -16,6 +16,7 @@
 //              O += P V  (TS: P bf16 in TMEM cols [0,64), V MN-major) -> [128,256)
 #include "../../include/bam.h"
 #include "common.cuh"
+#include "kernels.cuh"
 #include "tma.h"
 
 namespace bam {
@@ -610,9 +611,28 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
                           const int32_t* __restrict__ slot_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem_raw);
+  BAM_CTA_CLOCK_BEGIN();
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
-  const int bx = kRowMajor ? blockIdx.x : blockIdx.y, by = kRowMajor ? blockIdx.y : blockIdx.x;
+  int bx = kRowMajor ? blockIdx.x : blockIdx.y, by = kRowMajor ? blockIdx.y : blockIdx.x;
+  if (!kQPair && p.order_classes && !p.items) {
+    // class-major CTA order: linear CTA L walks the work classes of the
+    // heavy-first order, each class head-pair major (BamAttnFwdParams.order_classes)
+    const int npairs = kRowMajor ? gridDim.y : gridDim.x;
+    const int L = blockIdx.x + gridDim.x * blockIdx.y;   // the block scheduler's dispatch order
+    int lo = p.order_classes[0];
+#pragma unroll 1
+    for (int c = 1; c <= kOrderClasses; ++c) {
+      const int hi = p.order_classes[c];
+      if (L < npairs * hi) {
+        const int len = hi - lo, off = L - npairs * lo;
+        by = off / len;
+        bx = lo + (off - by * len);
+        break;
+      }
+      lo = hi;
+    }
+  }
   int jj[2], hh[2], n, slot;
   const int32_t* tl[2];
   // device-counted pairs / items (bam_plan_build): the grid is an upper bound
@@ -776,6 +796,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  BAM_CTA_CLOCK_END(n);
 }
 
 // ---------------------------------------------------------------------------
@@ -997,6 +1018,19 @@ __global__ void __launch_bounds__(128) combine_kernel(const BamAttnFwdParams p,
 }
 
 }  // namespace fwd
+
+// bam_set_cta_clock_buffer's forward half (this translation unit's symbol)
+int fwd_set_cta_clock(void* buf) {
+#ifdef BAM_CTA_CLOCK
+  BAM_CUDA_TRY(cudaMemcpyToSymbol(g_bam_cta_clock, &buf, sizeof(buf)));
+  return kOk;
+#else
+  (void)buf;
+  set_last_error("libbam built without -DBAM_CTA_CLOCK");
+  return BAM_UNSUPPORTED;
+#endif
+}
+
 }  // namespace bam
 
 using namespace bam;

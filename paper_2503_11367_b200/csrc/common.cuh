@@ -142,6 +142,40 @@ static __device__ unsigned long long* g_bam_trace = nullptr;   // per translatio
   } while (0)
 #endif
 
+// -DBAM_CTA_CLOCK builds record, per CTA of the attention kernels, {start, end}
+// %globaltimer ns, the SM id and the CTA's work count into a buffer installed
+// with bam_set_cta_clock_buffer (tools/cta_tail.py: the intra-GPU tail that a
+// persistent work queue could remove).
+#ifdef BAM_CTA_CLOCK
+static __device__ unsigned long long* g_bam_cta_clock = nullptr;   // per translation unit
+__device__ __forceinline__ unsigned long long bam_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BAM_CTA_CLOCK_BEGIN() const unsigned long long bam_cta_t0 = ::bam::bam_globaltimer()
+#define BAM_CTA_CLOCK_END(work)                                                           \
+  do {                                                                                    \
+    if (threadIdx.x == 0 && g_bam_cta_clock) {                                            \
+      uint32_t smid_;                                                                     \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                  \
+      unsigned long long* r_ =                                                            \
+          g_bam_cta_clock + 4 * (blockIdx.x + (size_t)gridDim.x * blockIdx.y);            \
+      r_[0] = bam_cta_t0;                                                                 \
+      r_[1] = ::bam::bam_globaltimer();                                                   \
+      r_[2] = smid_;                                                                      \
+      r_[3] = (unsigned long long)(work);                                                 \
+    }                                                                                     \
+  } while (0)
+#else
+#define BAM_CTA_CLOCK_BEGIN() \
+  do {                        \
+  } while (0)
+#define BAM_CTA_CLOCK_END(work) \
+  do {                          \
+  } while (0)
+#endif
+
 // ----------------------------------------------------------------------------- TMA
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

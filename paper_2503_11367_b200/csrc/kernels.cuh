@@ -7,6 +7,7 @@
 namespace bam {
 
 constexpr int kSortSmemMax = 16384;  // items sorted in one CTA's shared memory
+constexpr int kOrderClasses = 16;    // forward work classes (BamAttnFwdParams.order_classes)
 
 // mask_kernels.cu
 __global__ void list_count_kernel(const uint8_t* __restrict__ classes, int64_t nb,
@@ -26,6 +27,9 @@ __global__ void list_fill_cols_kernel(const uint8_t* __restrict__ classes, int64
 // first, ties by lower index); writes the keys and/or the index order
 __global__ void sort_smem_kernel(const int32_t* __restrict__ w, int64_t n, int64_t n_pad,
                                  uint64_t* __restrict__ sorted, int32_t* __restrict__ order);
+
+// attn_fwd.cu: the forward translation unit's half of bam_set_cta_clock_buffer
+int fwd_set_cta_clock(void* buf);
 
 namespace bwd {
 // attn_bwd.cu: CTA-pair step lists over CSC (or CSR) lists

@@ -7,6 +7,7 @@
 //   list_* kernels       CSR rows (fwd) / CSC columns (bwd) of non-skip tiles
 //   sort_smem_kernel     heavy-first processing orders (-count, index)
 //   pair_lists_dense_kernel  CTA-pair step lists (bwd) / query-block pairs (fwd)
+//   order_classes_kernel the forward's work classes over the heavy-first order
 //   fwd_pairs_kernel     compaction of the shared forward pairs and the
 //                        whole-row items of the others, with device counts
 //                        that the forward kernels read (grid = upper bound)
@@ -212,6 +213,35 @@ __global__ void __launch_bounds__(256) pair_lists_dense_kernel(
   }
 }
 
+// Geometric work classes over the heavy-first order (forward CTA order,
+// BamAttnFwdParams.order_classes): class(i) = floor(log2(n_max / n_i)) for the
+// tile count n_i of the i-th heaviest row, clamped to [0, kOrderClasses - 1]
+// (empty rows: the last class).  Classes are contiguous ranges of the order;
+// cls[c] = the first position of class >= c, cls[kOrderClasses] = n.
+__global__ void __launch_bounds__(1024) order_classes_kernel(const int32_t* __restrict__ cnt,
+                                                             const int32_t* __restrict__ order,
+                                                             int32_t n, int32_t* __restrict__ cls) {
+  const int n_max = cnt[order[0]];
+  auto klass = [&](int i) {
+    const int c = cnt[order[i]];
+    if (c <= 0) return kOrderClasses - 1;
+    const int k = 31 - __clz(n_max / c);   // floor(log2(n_max / c)), exact in integers
+    return k > kOrderClasses - 1 ? kOrderClasses - 1 : k;
+  };
+  if (threadIdx.x == 0) {
+    cls[0] = 0;
+    cls[kOrderClasses] = n;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int prev = i == 0 ? 0 : klass(i - 1), cur = klass(i);
+    for (int c = prev + 1; c <= cur; ++c) cls[c] = i;   // classes (prev, cur] start at i
+  }
+  // classes past the lightest present one are empty: they start at n
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int c = klass(n - 1) + 1; c < kOrderClasses; ++c) cls[c] = n;
+}
+
 static int64_t next_pow2(int64_t n) {
   int64_t p = 1;
   while (p < n) p <<= 1;
@@ -246,7 +276,8 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
                     p.col_cnt && p.col_off && p.col_tiles && p.fwd_order && p.bwd_order &&
                     p.slot_kb && p.slot_cnt && p.slot_off && p.slot_tiles && p.pair_shared &&
                     p.fwd_slot_q && p.fwd_slot_cnt && p.fwd_slot_off && p.fwd_slot_tiles &&
-                    p.fwd_shared && p.fwd_pair_ids && p.fwd_rest_items && p.counts,
+                    p.fwd_shared && p.fwd_pair_ids && p.fwd_rest_items && p.counts &&
+                    p.fwd_classes,
                 "bam_plan_build: null output buffer");
   BAM_CHECK_ARG(((uintptr_t)p.fwd_rest_items & 15) == 0,
                 "bam_plan_build: fwd_rest_items must be 16-byte aligned (int4 records)");
@@ -269,6 +300,7 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
   // heavy-first orders (LPT's sort key: -count, then index)
   if (int rc = heavy_first(p.col_cnt, nb, p.bwd_order, s)) return rc;
   if (int rc = heavy_first(p.row_cnt, nq, p.fwd_order, s)) return rc;
+  order_classes_kernel<<<1, 1024, 0, s>>>(p.row_cnt, p.fwd_order, nq, p.fwd_classes);
   // backward CTA-pair step lists over the columns, forward query-block pairs over the rows
   const int bp = (nb + 1) / 2, fp = (nq + 1) / 2;
   pair_lists_dense_kernel<true><<<bp, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.bwd_order, nb,

@@ -309,3 +309,42 @@ def test_head_major_kv_matches_token_major(Hq, Hkv):
     assert torch.equal(dk, dkh) and torch.equal(dv, dvh)
     with pytest.raises(ValueError, match="head-major"):
         A.attn_forward(q, k, v, plan, kv_head_major=True)
+
+
+def test_fwd_class_order_matches_head_pair_major():
+    """The forward's class-major CTA order (BamAttnFwdParams.order_classes):
+    the planner's geometric classes over the heavy-first order are the
+    floor(log2(n_max / n)) ranges, and the kernel walked in that order writes
+    bit-identical O / LSE to the head-pair-major order (it only reorders CTAs)."""
+    import os
+    from paper_2503_11367_b200 import attention as A, mask as M
+    from paper_2503_11367_b200.workloads import emu_interleave
+
+    mask = M.build_bitfield(emu_interleave(16 * 1024, seed=3))
+    plan = A.plan_for_mask(mask)
+    cnt = plan.row_cnt.cpu().numpy()[plan.fwd_order.cpu().numpy()]
+    assert np.all(np.diff(cnt) <= 0)
+    k_cls = np.array([min(int(cnt[0] // c).bit_length() - 1, 15) if c > 0 else 15 for c in cnt])
+    want = [int(np.searchsorted(k_cls, c, side="left")) for c in range(16)] + [len(cnt)]
+    got = plan.fwd_classes.cpu().tolist()
+    assert got == want, (got, want)
+    assert len(set(k_cls.tolist())) >= 3          # several classes present
+    T, Hq, Hkv = len(mask), 8, 2
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(5)
+    q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    old = os.environ.get("BAM_FWD_CLASS_ORDER")
+    try:
+        os.environ["BAM_FWD_CLASS_ORDER"] = "0"
+        o0, l0 = A.attn_forward(q, k, v, plan)
+        os.environ["BAM_FWD_CLASS_ORDER"] = "1"
+        o1, l1 = A.attn_forward(q, k, v, plan)
+    finally:
+        if old is None:
+            os.environ.pop("BAM_FWD_CLASS_ORDER", None)
+        else:
+            os.environ["BAM_FWD_CLASS_ORDER"] = old
+    torch.cuda.synchronize()
+    assert torch.equal(o0, o1) and torch.equal(l0, l1)
