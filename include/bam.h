@@ -175,8 +175,10 @@ typedef struct BamAttnFwdParams {
    * that size the grid, and CTAs past dev_counts[0] (pairs) or dev_counts[1]
    * (items) exit at once -- the plan needs no host synchronisation. */
   const int32_t* dev_counts;
-  /* Optional CTA order of the GQA head-pair kernel over whole rows (items ==
-   * NULL): order_classes[17] (bam_plan_build's fwd_classes) split the
+  /* Optional CTA order of the split-row kernels over whole rows (items == NULL:
+   * the GQA head-pair kernel with bam_plan_build's fwd_classes; the MHA
+   * query-block-pair kernel of bam_attn_fwd_qpairs with fwd_pair_classes):
+   * order_classes[17] split the
    * heavy-first order into geometric work classes [c, c+1) with c = floor(
    * log2(n_max / n)); the grid walks class by class, each class head-pair
    * major, so every head pair's heaviest rows start early and the kernel ends on
@@ -290,9 +292,11 @@ int bam_attn_fwd_qpairs(const BamAttnFwdParams* p, const int32_t* pair_ids, int3
  * col_off nb+1, fwd_order nq, bwd_order nb, slot_kb / slot_cnt 2P, slot_off
  * 2P+1, slot_tiles 2*n_tiles, pair_shared P, fwd_slot_q / fwd_slot_cnt 2F,
  * fwd_slot_off 2F+1, fwd_slot_tiles 2*n_tiles, fwd_shared F, fwd_pair_ids F,
- * fwd_rest_items 4*nq, counts 2, fwd_classes 17.  nb <= 16384 (2M tokens).
- * fwd_classes: the forward's geometric work classes over fwd_order
- * (BamAttnFwdParams.order_classes). */
+ * fwd_rest_items 4*nq, counts 2, fwd_classes 17, fwd_pair_w F, fwd_pair_classes
+ * 17.  nb <= 16384 (2M tokens).  fwd_classes: the forward's geometric work
+ * classes over fwd_order (BamAttnFwdParams.order_classes); fwd_pair_ids lists the
+ * shared pairs heavy-first by union length (fwd_pair_w), fwd_pair_classes their
+ * classes (the query-block-pair kernels' order_classes). */
 typedef struct BamPlan {
   const uint8_t* classes;   /* [nb, nb] from bam_classify */
   const int32_t* owner;     /* [nb] rank of each block (K3); may be NULL when world == 1 */
@@ -303,7 +307,8 @@ typedef struct BamPlan {
   int32_t *col_cnt, *col_off, *col_tiles, *fwd_order, *bwd_order;
   int32_t *slot_kb, *slot_cnt, *slot_off, *slot_tiles, *pair_shared;
   int32_t *fwd_slot_q, *fwd_slot_cnt, *fwd_slot_off, *fwd_slot_tiles, *fwd_shared;
-  int32_t *fwd_pair_ids, *fwd_rest_items, *counts, *fwd_classes;
+  int32_t *fwd_pair_ids, *fwd_rest_items, *counts, *fwd_classes, *fwd_pair_w,
+      *fwd_pair_classes;
 } BamPlan;
 int bam_plan_build(const BamPlan* plan, void* stream);
 

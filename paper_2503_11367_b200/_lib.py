@@ -40,7 +40,7 @@ PLAN_BUFFERS = ("k_row", "q_gid", "row_cnt", "row_off", "row_tiles", "col_cnt",
                 "col_off", "col_tiles", "fwd_order", "bwd_order", "slot_kb", "slot_cnt",
                 "slot_off", "slot_tiles", "pair_shared", "fwd_slot_q", "fwd_slot_cnt",
                 "fwd_slot_off", "fwd_slot_tiles", "fwd_shared", "fwd_pair_ids",
-                "fwd_rest_items", "counts", "fwd_classes")
+                "fwd_rest_items", "counts", "fwd_classes", "fwd_pair_w", "fwd_pair_classes")
 
 
 class BamPlan(ctypes.Structure):

@@ -63,8 +63,10 @@ class AttentionPlan:
     fwd_slot_tiles: torch.Tensor | None = None
     fwd_rest_items: torch.Tensor | None = None
     counts: torch.Tensor | None = None
-    # geometric work classes over fwd_order: the head-pair kernel's CTA order
+    # geometric work classes over fwd_order: the head-pair kernel's CTA order; over
+    # fwd_pair_ids (shared pairs heavy-first): the query-block-pair kernel's
     fwd_classes: torch.Tensor | None = None
+    fwd_pair_classes: torch.Tensor | None = None
     row_cnt: torch.Tensor | None = None
     col_cnt: torch.Tensor | None = None
 
@@ -82,7 +84,7 @@ def _plan_sizes(nb: int, nq: int, n_tiles: int) -> dict:
             "slot_off": 2 * P + 1, "slot_tiles": 2 * t, "pair_shared": P, "fwd_slot_q": 2 * F,
             "fwd_slot_cnt": 2 * F, "fwd_slot_off": 2 * F + 1, "fwd_slot_tiles": 2 * t,
             "fwd_shared": F, "fwd_pair_ids": F, "fwd_rest_items": 4 * nq, "counts": 2,
-            "fwd_classes": 17}
+            "fwd_classes": 17, "fwd_pair_w": F, "fwd_pair_classes": 17}
 
 
 def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, nq: int,
@@ -116,7 +118,8 @@ def native_plan(desc: torch.Tensor, classes: torch.Tensor, W: torch.Tensor, *, n
         fwd_pair_ids=views["fwd_pair_ids"], fwd_slot_q=views["fwd_slot_q"],
         fwd_slot_off=views["fwd_slot_off"], fwd_slot_tiles=views["fwd_slot_tiles"],
         fwd_rest_items=views["fwd_rest_items"].view(nq, 4), counts=views["counts"],
-        fwd_classes=views["fwd_classes"], row_cnt=views["row_cnt"], col_cnt=views["col_cnt"])
+        fwd_classes=views["fwd_classes"], fwd_pair_classes=views["fwd_pair_classes"],
+        row_cnt=views["row_cnt"], col_cnt=views["col_cnt"])
 
 
 def build_plan(desc: torch.Tensor, classes: torch.Tensor | None = None,
@@ -314,6 +317,8 @@ def _launch_fwd(p, plan: AttentionPlan, schedule, pair_heads: bool, flagged: boo
             _lib.call("bam_attn_fwd_combine", p, schedule.combine.data_ptr(),
                       int(schedule.combine.shape[0]))
         return
+    if p.order_classes and plan.fwd_pair_classes is not None:
+        p.order_classes = plan.fwd_pair_classes.data_ptr()
     _lib.call(entry, p, plan.fwd_pair_ids.data_ptr(), int(plan.fwd_pair_ids.shape[0]),
               plan.fwd_slot_q.data_ptr(), plan.fwd_slot_off.data_ptr(),
               plan.fwd_slot_tiles.data_ptr())

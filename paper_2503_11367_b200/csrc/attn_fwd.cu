@@ -615,9 +615,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
   const uint32_t warp = warp_id(), lane = lane_id();
   const int nh = p.nh > 0 ? p.nh : p.Hq;
   int bx = kRowMajor ? blockIdx.x : blockIdx.y, by = kRowMajor ? blockIdx.y : blockIdx.x;
-  if (!kQPair && p.order_classes && !p.items) {
+  if (p.order_classes && (kQPair || !p.items)) {
     // class-major CTA order: linear CTA L walks the work classes of the
-    // heavy-first order, each class head-pair major (BamAttnFwdParams.order_classes)
+    // heavy-first order (rows, or shared query-block pairs), each class head-pair
+    // (head) major (BamAttnFwdParams.order_classes)
     const int npairs = kRowMajor ? gridDim.y : gridDim.x;
     const int L = blockIdx.x + gridDim.x * blockIdx.y;   // the block scheduler's dispatch order
     int lo = p.order_classes[0];

@@ -8,6 +8,7 @@
 //   sort_smem_kernel     heavy-first processing orders (-count, index)
 //   pair_lists_dense_kernel  CTA-pair step lists (bwd) / query-block pairs (fwd)
 //   order_classes_kernel the forward's work classes over the heavy-first order
+//                        (query blocks; shared query-block pairs, sorted heavy-first)
 //   fwd_pairs_kernel     compaction of the shared forward pairs and the
 //                        whole-row items of the others, with device counts
 //                        that the forward kernels read (grid = upper bound)
@@ -242,6 +243,14 @@ __global__ void __launch_bounds__(1024) order_classes_kernel(const int32_t* __re
     for (int c = klass(n - 1) + 1; c < kOrderClasses; ++c) cls[c] = n;
 }
 
+// weight of forward query-block pair pr: its union list length if shared, else 0
+__global__ void pair_weights_kernel(const int32_t* __restrict__ shared,
+                                    const int32_t* __restrict__ slot_cnt, int32_t npairs,
+                                    int32_t* __restrict__ w) {
+  const int pr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pr < npairs) w[pr] = shared[pr] ? slot_cnt[2 * pr] : 0;
+}
+
 static int64_t next_pow2(int64_t n) {
   int64_t p = 1;
   while (p < n) p <<= 1;
@@ -277,7 +286,7 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
                     p.slot_kb && p.slot_cnt && p.slot_off && p.slot_tiles && p.pair_shared &&
                     p.fwd_slot_q && p.fwd_slot_cnt && p.fwd_slot_off && p.fwd_slot_tiles &&
                     p.fwd_shared && p.fwd_pair_ids && p.fwd_rest_items && p.counts &&
-                    p.fwd_classes,
+                    p.fwd_classes && p.fwd_pair_w && p.fwd_pair_classes,
                 "bam_plan_build: null output buffer");
   BAM_CHECK_ARG(((uintptr_t)p.fwd_rest_items & 15) == 0,
                 "bam_plan_build: fwd_rest_items must be 16-byte aligned (int4 records)");
@@ -319,6 +328,13 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
                                                     p.fwd_slot_tiles, p.fwd_shared);
   fwd_pairs_kernel<<<1, 1024, 0, s>>>(p.fwd_shared, p.fwd_slot_q, p.row_cnt, fp, p.fwd_pair_ids,
                                       reinterpret_cast<int4*>(p.fwd_rest_items), p.counts);
+  // shared pairs heavy-first by union length (the others weigh 0 and sort last, so
+  // the first counts[0] entries are the same pairs), and their work classes
+  pair_weights_kernel<<<(fp + 255) / 256, 256, 0, s>>>(p.fwd_shared, p.fwd_slot_cnt, fp,
+                                                       p.fwd_pair_w);
+  BAM_LAUNCH_CHECK();
+  if (int rc = heavy_first(p.fwd_pair_w, fp, p.fwd_pair_ids, s)) return rc;
+  order_classes_kernel<<<1, 1024, 0, s>>>(p.fwd_pair_w, p.fwd_pair_ids, fp, p.fwd_pair_classes);
   BAM_LAUNCH_CHECK();
   return kOk;
 }

@@ -329,22 +329,34 @@ def test_fwd_class_order_matches_head_pair_major():
     got = plan.fwd_classes.cpu().tolist()
     assert got == want, (got, want)
     assert len(set(k_cls.tolist())) >= 3          # several classes present
-    T, Hq, Hkv = len(mask), 8, 2
+    # shared query-block pairs (MHA): heavy-first by union length, then classes
+    n_sh = int(plan.counts[0])
+    assert n_sh > 1
+    F = plan.fwd_pair_ids.shape[0]
+    pid = plan.fwd_pair_ids.cpu().numpy()
+    slot_off = plan.fwd_slot_off.cpu().numpy()
+    w = np.array([slot_off[2 * pr + 1] - slot_off[2 * pr] for pr in pid[:n_sh]])
+    assert np.all(np.diff(w) <= 0) and w[-1] > 0
+    wk = [min(int(w[0] // c).bit_length() - 1, 15) for c in w] + [15] * (F - n_sh)
+    want = [int(np.searchsorted(np.array(wk), c, side="left")) for c in range(16)] + [F]
+    assert plan.fwd_pair_classes.cpu().tolist() == want
     dev = torch.device("cuda")
-    g = torch.Generator(device=dev).manual_seed(5)
-    q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
-    k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
-    v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
-    old = os.environ.get("BAM_FWD_CLASS_ORDER")
-    try:
-        os.environ["BAM_FWD_CLASS_ORDER"] = "0"
-        o0, l0 = A.attn_forward(q, k, v, plan)
-        os.environ["BAM_FWD_CLASS_ORDER"] = "1"
-        o1, l1 = A.attn_forward(q, k, v, plan)
-    finally:
-        if old is None:
-            os.environ.pop("BAM_FWD_CLASS_ORDER", None)
-        else:
-            os.environ["BAM_FWD_CLASS_ORDER"] = old
-    torch.cuda.synchronize()
-    assert torch.equal(o0, o1) and torch.equal(l0, l1)
+    for Hq, Hkv in ((8, 2), (2, 2)):     # GQA head pairs; MHA query-block pairs + rest
+        T = len(mask)
+        g = torch.Generator(device=dev).manual_seed(5)
+        q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+        k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+        v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+        old = os.environ.get("BAM_FWD_CLASS_ORDER")
+        try:
+            os.environ["BAM_FWD_CLASS_ORDER"] = "0"
+            o0, l0 = A.attn_forward(q, k, v, plan)
+            os.environ["BAM_FWD_CLASS_ORDER"] = "1"
+            o1, l1 = A.attn_forward(q, k, v, plan)
+        finally:
+            if old is None:
+                os.environ.pop("BAM_FWD_CLASS_ORDER", None)
+            else:
+                os.environ["BAM_FWD_CLASS_ORDER"] = old
+        torch.cuda.synchronize()
+        assert torch.equal(o0, o1) and torch.equal(l0, l1), (Hq, Hkv)
