@@ -56,10 +56,8 @@ constexpr int kBwdPChunks = 2;
 // splits, exact to ~2^-24) from a per-step bias tile [64 queries x 16] times a
 // constant ones tile [128 keys x 16], so the compute warps need no per-query
 // values -- the broadcast loads that fed them were ~12% of the shared-memory
-// port traffic, the kernel's binding resource (0: broadcast LDS.128)
-#ifndef BAM_BWD_BIAS
-#define BAM_BWD_BIAS 1
-#endif
+// port traffic, the kernel's binding resource (measured +1.3%,
+// profiles/r02/ab_bwd_bias.txt)
 #ifndef BAM_DQ_SLEEP_NS
 #define BAM_DQ_SLEEP_NS 64
 #endif
@@ -77,11 +75,9 @@ constexpr uint32_t kColDV = 0, kColDK = 128, kColK = 256, kColV = 320, kColS = 3
 struct Stage {
   alignas(1024) uint8_t q[kHalfBytes];
   alignas(1024) uint8_t dout[kHalfBytes];
-#if BAM_BWD_BIAS
   // bias B operands [64 queries x 16] bf16, SWIZZLE_NONE K-major core matrices
   // ([k chunk][row group][8 rows][8]): [0] -lse/c, [1] -D as (hi, mid, lo, 0...)
   alignas(1024) __nv_bfloat16 bias[2][64 * 16];
-#endif
 };
 
 struct Smem {
@@ -90,11 +86,7 @@ struct Smem {
   alignas(1024) uint8_t ds[kDsBytes];
   Stage st[kStages];
   alignas(128) float dq_stage[64 * 128];  // dQ tile [64 queries][128 d] fp32 for the bulk reduce
-#if BAM_BWD_BIAS
   alignas(128) __nv_bfloat16 ones[128 * 16];  // A operand [128 keys x 16]: 1 in k = 0, 1, 2
-#else
-  alignas(16) float ld[kStages][128];   // per stage: (lse * log2e, delta) pairs, 64 queries
-#endif
   uint64_t bar_kv, bar_full[kStages], bar_empty[kStages];
   uint64_t bar_s_full, bar_p_ready[kBwdPChunks], bar_mma_done, bar_dq_full, bar_dq_empty;
   uint64_t bar_kvt, bar_dp_full, bar_ds_ready;
@@ -118,36 +110,21 @@ __device__ __forceinline__ uint4 bias_chunk(float x) {
                     uint32_t(__bfloat16_as_ushort(lo)), 0u, 0u);
 }
 
-// P = 2^(S c - lse) for a pair of queries (packed FFMA2, exponentials on MUFU:
+// P = 2^(S c - lse) for a pair of queries (packed FMUL2, exponentials on MUFU:
 // the backward's MUFU is ~25% busy, a polynomial share measured slower), masked by
-// the PARTIAL-tile allow bits.  With BAM_BWD_BIAS the S columns already hold
-// S - lse / c and lse0 = lse1 = 0.
-__device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, float lse0, float lse1,
-                                         float sc, int i2, uint32_t allow) {
-#if BAM_BWD_BIAS
-  (void)lse0;
-  (void)lse1;
+// the PARTIAL-tile allow bits.  The S columns already hold S - lse / c (bias MMA).
+__device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, float sc, int i2,
+                                         uint32_t allow) {
   const float2 x = fmul2(make_float2(__uint_as_float(s0), __uint_as_float(s1)),
                          make_float2(sc, sc));
-#else
-  const float2 x = ffma2(make_float2(__uint_as_float(s0), __uint_as_float(s1)),
-                         make_float2(sc, sc), make_float2(-lse0, -lse1));
-#endif
   float2 p = make_float2(ex2(x.x), ex2(x.y));
   p.x = (allow >> (2 * i2)) & 1 ? p.x : 0.f;
   p.y = (allow >> (2 * i2 + 1)) & 1 ? p.y : 0.f;
   return p;
 }
-// dS = P (dP - D) for the same pair
-__device__ __forceinline__ float2 ds_pair(float2 p, uint32_t dp0, uint32_t dp1, float D0, float D1) {
-#if BAM_BWD_BIAS
-  (void)D0;
-  (void)D1;
-  return fmul2(p, make_float2(__uint_as_float(dp0), __uint_as_float(dp1)));  // dP - D in TMEM
-#else
-  return fmul2(p, fadd2(make_float2(__uint_as_float(dp0), __uint_as_float(dp1)),
-                        make_float2(-D0, -D1)));
-#endif
+// dS = P (dP - D) for the same pair (the dP columns hold dP - D: bias MMA)
+__device__ __forceinline__ float2 ds_pair(float2 p, uint32_t dp0, uint32_t dp1) {
+  return fmul2(p, make_float2(__uint_as_float(dp0), __uint_as_float(dp1)));
 }
 
 struct StepInfo {
@@ -210,7 +187,7 @@ __global__ void __maxnreg__(128)
     if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // SWIZZLE_128B needs 1024-B alignment
     mbar_init(&sm.bar_kv, 1);
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(&sm.bar_full[i], BAM_BWD_BIAS ? 2 : 1);  // + the bias tile's arrival
+      mbar_init(&sm.bar_full[i], 2);  // TMA bytes + the bias tile's arrival
       mbar_init(&sm.bar_empty[i], shared ? 2 : 1);  // shared: both CTAs' MMAs release a stage
     }
     mbar_init(&sm.bar_s_full, 1);
@@ -257,7 +234,7 @@ __global__ void __maxnreg__(128)
         if (s >= kStages) mbar_wait_sleep(&sm.bar_empty[st], ((s / kStages) - 1) & 1);
         BAM_TRACE_EV(trace_cta && leader, 10, s);
         Stage& S = sm.st[st];
-        mbar_expect_tx_w(&sm.bar_full[st], 2 * kHalfBytes + (BAM_BWD_BIAS ? 0 : 512), leader);
+        mbar_expect_tx_w(&sm.bar_full[st], 2 * kHalfBytes, leader);
         if (shared) {  // this CTA loads column box `crank` of Q and dO for both CTAs
           const uint32_t off = crank * (kHalfBytes / 2);
           tma_load_3d_mc_w(&tm_q, &sm.bar_full[st], S.q + off, crank * 64, si.h, row0, 0x3,
@@ -271,7 +248,6 @@ __global__ void __maxnreg__(128)
           tma_load_3d_w(&tm_do, &sm.bar_full[st], S.dout + kHalfBytes / 2, 64, si.h, row0,
                         leader);
         }
-#if BAM_BWD_BIAS
         {  // bias tiles: lane l writes queries 2l, 2l+1 (k chunk 0; chunk 1 stays zero)
           const float* ld = p.delta + (int64_t)si.h * 2 * Tq + row0;
           const float2 lse2 = *reinterpret_cast<const float2*>(ld + 2 * lane);
@@ -288,12 +264,6 @@ __global__ void __maxnreg__(128)
           __syncwarp();
           if (leader) mbar_arrive(&sm.bar_full[st]);
         }
-#else
-        bulk_load_w(sm.ld[st], p.delta + (int64_t)si.h * 2 * Tq + row0, 256, &sm.bar_full[st],
-                    leader);
-        bulk_load_w(sm.ld[st] + 64, p.delta + (int64_t)si.h * 2 * Tq + Tq + row0, 256,
-                    &sm.bar_full[st], leader);
-#endif
       }
     }
   } else if (warp == kWarpMMA) {
@@ -310,12 +280,10 @@ __global__ void __maxnreg__(128)
       const uint64_t d_q0mn = sdesc_sw128(smem_u32(sm.st[0].q), kHalfBytes / 2, 1024);
       const uint64_t d_ds0 = sdesc_sw128(smem_u32(sm.ds), 16, 1024);
       constexpr uint32_t kStage16 = sizeof(Stage) >> 4, kDo16 = kHalfBytes >> 4;
-#if BAM_BWD_BIAS
       // ones [128 x 16]: k-chunk stride 16 row groups x 128 B; bias [64 x 16]: 8 x 128 B
       const uint64_t d_ones = sdesc_noswz(smem_u32(sm.ones), 2048, 128);
       const uint64_t d_bias0 = sdesc_noswz(smem_u32(sm.st[0].bias[0]), 1024, 128);
       constexpr uint32_t kBias16 = (64 * 16 * 2) >> 4;
-#endif
       const uint32_t tK = tmem + kColK, tV = tmem + kColV, tS = tmem + kColS, tDP = tmem + kColDP;
       mbar_wait(&sm.bar_kvt, 0);  // K / V rows stored into TMEM by the compute warps
       // S^T(s) = K Q^T (A = K from TMEM) -> S; S(s) overwrites P^T(s-1), the A operand of
@@ -326,13 +294,11 @@ __global__ void __maxnreg__(128)
         BAM_TRACE_EV(trace_cta && leader, 11, s);
         tc_fence_after();
         const uint64_t dq = d_q0 + st * kStage16;
-#if BAM_BWD_BIAS
         mma_ss_w(tS, d_ones, d_bias0 + st * kStage16, id_s, 0, leader);   // S := -lse / c
-#endif
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
-          mma_ts_w(tS, tK + 8 * kk, dq + kq, id_s, BAM_BWD_BIAS || kk > 0, leader);
+          mma_ts_w(tS, tK + 8 * kk, dq + kq, id_s, 1, leader);   // accumulates onto the bias
         }
         tc_commit_w(&sm.bar_s_full, leader);
       };
@@ -343,13 +309,11 @@ __global__ void __maxnreg__(128)
         BAM_TRACE_EV(trace_cta && leader, 1, s);
         tc_fence_after();
         const uint64_t ddo = d_q0 + st * kStage16 + kDo16;
-#if BAM_BWD_BIAS
         mma_ss_w(tDP, d_ones, d_bias0 + st * kStage16 + kBias16, id_s, 0, leader);   // dP := -D
-#endif
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t kq = ((kk >> 2) * (kHalfBytes / 2) + (kk & 3) * 32) >> 4;
-          mma_ts_w(tDP, tV + 8 * kk, ddo + kq, id_s, BAM_BWD_BIAS || kk > 0, leader);
+          mma_ts_w(tDP, tV + 8 * kk, ddo + kq, id_s, 1, leader);
         }
         tc_commit_w(&sm.bar_dp_full, leader);
         BAM_TRACE_EV(trace_cta && leader, 12, s);
@@ -430,7 +394,6 @@ __global__ void __maxnreg__(128)
         BAM_TMEM_ST32(tmem + lane_base + (c == 0 ? kColK : kColV) + 32 * hb, w);
       }
       tmem_wait_st();
-#if BAM_BWD_BIAS
       {  // ones tile (thread t: row t % 128, k chunk t / 128) and the bias tiles' zero chunk
         const int t = c * 128 + r;
         const uint32_t one = 0x3F80u | (0x3F80u << 16);   // bf16 1.0 pairs
@@ -444,7 +407,6 @@ __global__ void __maxnreg__(128)
         }
         fence_async_smem();
       }
-#endif
       tc_fence_before();
       mbar_arrive(&sm.bar_kvt);
     }
@@ -468,15 +430,6 @@ __global__ void __maxnreg__(128)
           allow |= uint32_t(bam_allowed(__ldg(p.desc + qg0 + i), qg0 + i, dk, kg)) << i;
       }
       tmem_wait_ld();
-      // this warpgroup's 32 queries: lse*log2e at ld[32c ..], D at ld[64 + 32c ..]
-#if BAM_BWD_BIAS
-      // lse / D are already folded into the S / dP columns by the bias MMAs
-      constexpr float lse_s[32] = {}, d_s[32] = {};
-#else
-      // (broadcast loads: every lane reads the same 16-B pairs)
-      const float* lse_s = sm.ld[s % kStages] + c * 32;
-      const float* d_s = sm.ld[s % kStages] + 64 + c * 32;
-#endif
       // P^T over this warpgroup's own S columns, released in kBwdPChunks chunks
 #pragma unroll
       for (int j = 0; j < kBwdPChunks; ++j) {
@@ -485,8 +438,7 @@ __global__ void __maxnreg__(128)
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
           const int i2 = j * kPer + u;
-          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], lse_s[2 * i2],
-                                   lse_s[2 * i2 + 1], scale_log2, i2, allow);
+          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], scale_log2, i2, allow);
           sr[2 * i2] = __float_as_uint(pp.x);
           sr[2 * i2 + 1] = __float_as_uint(pp.y);
           pk[u] = pack_bf16(pp.x, pp.y);
@@ -511,8 +463,7 @@ __global__ void __maxnreg__(128)
       for (int i2 = 0; i2 < 16; ++i2) {
         const float2 ds = ds_pair(make_float2(__uint_as_float(sr[2 * i2]),
                                               __uint_as_float(sr[2 * i2 + 1])),
-                                  dr[2 * i2], dr[2 * i2 + 1], d_s[2 * i2],
-                                  d_s[2 * i2 + 1]);
+                                  dr[2 * i2], dr[2 * i2 + 1]);
         dsk[i2] = pack_bf16(ds.x, ds.y);
       }
       // dS^T row r, query columns 32c .. 32c+31 (the A operand of dK, B of dQ^T)
