@@ -698,6 +698,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         tma_load_3d_w(&tm_q, &sm.bar_q, sm.q[i] + kTileBytes / 2, 64, hh[i], jj[i] * 128, leader);
       }
       uint64_t ready = 0;  // CP overlap: ranks whose K/V rows are known to have landed
+#ifdef BAM_CTA_CLOCK
+      unsigned long long flag_wait_ns = 0;
+#endif
       for (int t = 0; t < n; ++t) {
         const int st = t & 1;
         const int kblk = p.k_row[tiles[t] >> 2];
@@ -705,12 +708,18 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         if (p.kv_ready) {
           const int owner = kblk / p.kv_rows_per_rank;
           if (owner != p.kv_rank && !((ready >> owner) & 1)) {
+#ifdef BAM_CTA_CLOCK
+            const unsigned long long w0 = bam_globaltimer();
+#endif
             if (lane == 0)
               wait_flag_geq(p.kv_ready + (p.kv_head_major ? owner * p.Hkv + hkv : owner),
                             p.kv_epoch);
             __syncwarp();
             fence_proxy_async_global();  // the copy engine's data before the TMA reads
             ready |= 1ull << owner;
+#ifdef BAM_CTA_CLOCK
+            flag_wait_ns += bam_globaltimer() - w0;
+#endif
           }
         }
         if (t >= 2) mbar_wait_sleep(&sm.bar_k_empty[st], ((t >> 1) - 1) & 1);
@@ -722,6 +731,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st], 0, hkv, krow, leader);
         tma_load_3d_w(&tm_v, &sm.bar_v_full[st], sm.v[st] + kTileBytes / 2, 64, hkv, krow, leader);
       }
+#ifdef BAM_CTA_CLOCK
+      if (leader) BAM_CTA_CLOCK_FLAG_WAIT(flag_wait_ns);
+#endif
     }
   } else if (warp == kWarpMma) {
     const uint32_t leader = elect_one();

@@ -143,9 +143,10 @@ static __device__ unsigned long long* g_bam_trace = nullptr;   // per translatio
 #endif
 
 // -DBAM_CTA_CLOCK builds record, per CTA of the attention kernels, {start, end}
-// %globaltimer ns, the SM id and the CTA's work count into a buffer installed
-// with bam_set_cta_clock_buffer (tools/cta_tail.py: the intra-GPU tail that a
-// persistent work queue could remove).
+// %globaltimer ns, the SM id, the CTA's work count and (forward) the ns its TMA
+// warp spent waiting on CP arrival flags into a buffer installed with
+// bam_set_cta_clock_buffer (tools/cta_tail.py: the intra-GPU tail that a
+// persistent work queue could remove; the exposed exchange).
 #ifdef BAM_CTA_CLOCK
 static __device__ unsigned long long* g_bam_cta_clock = nullptr;   // per translation unit
 __device__ __forceinline__ unsigned long long bam_globaltimer() {
@@ -160,14 +161,22 @@ __device__ __forceinline__ unsigned long long bam_globaltimer() {
       uint32_t smid_;                                                                     \
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                  \
       unsigned long long* r_ =                                                            \
-          g_bam_cta_clock + 4 * (blockIdx.x + (size_t)gridDim.x * blockIdx.y);            \
+          g_bam_cta_clock + 8 * (blockIdx.x + (size_t)gridDim.x * blockIdx.y);            \
       r_[0] = bam_cta_t0;                                                                 \
       r_[1] = ::bam::bam_globaltimer();                                                   \
       r_[2] = smid_;                                                                      \
       r_[3] = (unsigned long long)(work);                                                 \
     }                                                                                     \
   } while (0)
+#define BAM_CTA_CLOCK_FLAG_WAIT(ns)                                                       \
+  do {                                                                                    \
+    if (g_bam_cta_clock)                                                                  \
+      g_bam_cta_clock[8 * (blockIdx.x + (size_t)gridDim.x * blockIdx.y) + 4] = (ns);      \
+  } while (0)
 #else
+#define BAM_CTA_CLOCK_FLAG_WAIT(ns) \
+  do {                              \
+  } while (0)
 #define BAM_CTA_CLOCK_BEGIN() \
   do {                        \
   } while (0)
