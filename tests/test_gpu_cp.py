@@ -449,7 +449,16 @@ def test_native_planner_matches_host_statement(policy, world):
         assert torch.equal(at.fwd_slot_tiles[:int(foff[-1])], ftiles[:int(foff[-1])])
         assert fsh_d.cpu().tolist() == [int(x) for x in fsh]
         n_pairs, n_rest = at.counts.cpu().tolist()
-        assert at.fwd_pair_ids[:n_pairs].cpu().tolist() == [pr for pr in range(fp) if fsh[pr]]
+        # shared pairs heavy-first by union length, ties by pair index (fwd_pair_w), and
+        # their geometric work classes (the query-block-pair kernel's CTA order)
+        fcnt_h = fcnt.cpu().tolist()
+        want = sorted((pr for pr in range(fp) if fsh[pr]), key=lambda pr: (-fcnt_h[2 * pr], pr))
+        assert at.fwd_pair_ids[:n_pairs].cpu().tolist() == want
+        w_sorted = [fcnt_h[2 * pr] for pr in want] + [0] * (fp - n_pairs)
+        kc = [min(int(w_sorted[0] // c).bit_length() - 1, 15) if c > 0 else 15
+              for c in w_sorted] if n_pairs else [15] * fp
+        assert at.fwd_pair_classes.cpu().tolist() == [
+            next((i for i, x in enumerate(kc) if x >= c), fp) for c in range(16)] + [fp]
         rest = [j for pr in range(fp) if not fsh[pr] for j in fslot[pr].tolist() if j >= 0]
         assert n_rest == len(rest)
         items = at.fwd_rest_items[:n_rest].cpu().tolist()
