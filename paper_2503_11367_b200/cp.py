@@ -489,13 +489,13 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     """K/V all-gather + the rank's attention forward.
 
     transport "ce" (what "auto" picks when peer memory works): copy-engine
-    pulls from symmetric memory; for GQA with one head group the forward
-    starts on this rank's own key tiles at once and waits per tile on
-    per-(rank, KV head) arrival flags for the rest (no SM is spent on the
-    transfer, so the spin cannot starve it).  Otherwise (MHA, ``groups`` > 1
-    or "nccl") K/V travel per KV-head group on a side stream and the forward
-    of group g starts when its K/V have landed, overlapping the gather of
-    group g+1.
+    pulls from symmetric memory; with one head group the forward (GQA head
+    pairs, or MHA query-block pairs + whole rows) starts on this rank's own key
+    tiles at once and waits per tile on per-(rank, KV head) arrival flags for
+    the rest (no SM is spent on the transfer, so the spin cannot starve it).
+    Otherwise (``groups`` > 1 or "nccl") K/V travel per KV-head group on a side
+    stream and the forward of group g starts when its K/V have landed,
+    overlapping the gather of group g+1.
 
     ``timer=(start, end)`` CUDA events recorded right around the forward
     kernel launches (kernel-only time, no exchange barrier inside).
@@ -516,10 +516,10 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     gathered, events = [], []
     hg = _head_groups(Hkv, groups)
     ex = plan.exchange(Hkv, d, k_loc.device, group) if transport == "ce" else None
-    if ex is not None and len(hg) == 1 and grp % 2 == 0:
-        # GQA: the forward starts on this rank's key tiles while the copy engines pull the
-        # peers' K/V.  MHA runs query-block pairs whose union lists are not local-first; it
-        # measured slower than gathering first (config 2, N=4: 3269 vs 3395 TFLOP/s)
+    if ex is not None and len(hg) == 1:
+        # the forward starts on this rank's key tiles while the copy engines pull the
+        # peers' K/V: every tile list is local-first (CSR rows and, for MHA, the
+        # query-block pairs' union lists), so no CTA waits before its local tiles
         comm.wait_stream(cur)
         with torch.cuda.stream(comm):
             k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(

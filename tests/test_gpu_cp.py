@@ -353,6 +353,79 @@ def test_cp_emulated_world8_config4_overlapped_forward():
     assert rel_l2(dv_sum, dv_1) < 1e-2 and (dv_sum - dv_1).abs().max().item() < 2e-2
 
 
+def test_cp_emulated_mha_overlapped_forward():
+    """MHA under the overlapped copy-engine forward: the query-block-pair kernel's
+    union lists are local-first (bam_plan_build), so its CTAs start on this rank's
+    key tiles and wait per tile on the per-(rank, head) arrival flags while the
+    peers' rows land by DMA after the launch; O and dQ per rank against the
+    single-GPU path, the dK/dV partials summed over the ranks against its dK/dV."""
+    from paper_2503_11367_b200 import _lib
+    from paper_2503_11367_b200 import attention as A
+    from paper_2503_11367_b200 import cp
+    from paper_2503_11367_b200 import mask as M
+
+    world, Hq, Hkv = 4, 4, 4
+    mask = M.build_bitfield([("image", 2048), ("text", 3072), ("img1", 1024), ("text", 2048)])
+    d_desc = mask.device_descriptors()
+    T = d_desc.shape[0]
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(11)
+    qd, kd, vd, dod = (torch.randn(T, h, 128, device=dev, generator=g, dtype=torch.bfloat16)
+                       for h in (Hq, Hkv, Hkv, Hq))
+    full = A.plan_for_mask(mask)
+    o_1, lse_1 = A.attn_forward(qd, kd, vd, full)
+    dq_1, dk_1, dv_1 = A.attn_backward(qd, kd, vd, o_1, lse_1, dod, full, dkv_fp32=True)
+    dk_sum = torch.zeros(T, Hkv, 128, device=dev)
+    dv_sum = torch.zeros_like(dk_sum)
+    side = torch.cuda.Stream()
+    n_pairs_seen = 0
+    for rank in range(world):
+        plan = cp.make_cp_plan(d_desc, world, rank, "lpt")
+        lay = plan.layout
+        n_pairs_seen += int(plan.attn.counts[0])
+        rows = lay.max_blocks * BLOCK
+        idx = (lay.k_row.to(torch.int64)[:, None] * BLOCK +
+               torch.arange(BLOCK, device=dev)[None, :]).reshape(-1)
+        k_src = torch.zeros(Hkv, world * rows, 128, dtype=torch.bfloat16, device=dev)
+        v_src = torch.zeros_like(k_src)
+        k_src[:, idx] = kd.transpose(0, 1)
+        v_src[:, idx] = vd.transpose(0, 1)
+        k_all, v_all = torch.zeros_like(k_src), torch.zeros_like(v_src)
+        mine = slice(rank * rows, (rank + 1) * rows)
+        k_all[:, mine] = k_src[:, mine]
+        v_all[:, mine] = v_src[:, mine]
+        k_src_h, v_src_h = k_src.cpu().pin_memory(), v_src.cpu().pin_memory()
+        flags = torch.zeros(world * Hkv, dtype=torch.int32, device=dev)
+        epoch = 5 + rank
+        q_loc, do_loc = cp.shard_rows(qd, dod, layout=lay)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(5_000_000)         # the peers' rows land after the launch
+            for peer in range(world):
+                if peer == rank:
+                    continue
+                sl = slice(peer * rows, (peer + 1) * rows)
+                for h in range(Hkv):
+                    k_all[h, sl].copy_(k_src_h[h, sl], non_blocking=True)
+                    v_all[h, sl].copy_(v_src_h[h, sl], non_blocking=True)
+                    _lib.call("bam_stream_write_i32", flags[peer * Hkv + h:].data_ptr(), epoch)
+        o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn,
+                                kv_ready=(flags, epoch, rank, lay.max_blocks), kv_head_major=True)
+        torch.cuda.synchronize()
+        ws = A.BackwardWorkspace(q_loc, o, lse, do_loc, plan.attn, None)
+        dk_all, dv_all = ws.main(k_all, v_all, kv_head_major=True)
+        dq = ws.finalize()
+        dk_sum += dk_all[idx]
+        dv_sum += dv_all[idx]
+        pos = (lay.local_blocks.to(torch.int64)[:, None] * BLOCK +
+               torch.arange(BLOCK, device=dev)[None, :]).reshape(-1)
+        assert (o.float() - o_1[pos].float()).abs().max().item() < 2e-2, rank
+        assert rel_l2(o, o_1[pos]) < 1e-2 and rel_l2(dq, dq_1[pos]) < 1e-2, rank
+    assert n_pairs_seen > 0                       # the query-block-pair kernel ran
+    assert rel_l2(dk_sum, dk_1) < 1e-2 and (dk_sum - dk_1).abs().max().item() < 2e-2
+    assert rel_l2(dv_sum, dv_1) < 1e-2 and (dv_sum - dv_1).abs().max().item() < 2e-2
+
+
 @pytest.mark.parametrize("policy,world", [("lpt", 1), ("lpt", 4), ("zigzag", 3), ("lpt", 8)])
 def test_native_planner_matches_host_statement(policy, world):
     """bam_plan_build (one launch sequence, no host sync) against a host
@@ -446,7 +519,14 @@ def test_native_planner_matches_host_statement(policy, world):
                   at.fwd_order.data_ptr(), nq, fq.data_ptr(), fcnt.data_ptr(), foff.data_ptr(),
                   ftiles.data_ptr(), fsh_d.data_ptr())
         assert torch.equal(at.fwd_slot_q, fq) and torch.equal(at.fwd_slot_off, foff)
-        assert torch.equal(at.fwd_slot_tiles[:int(foff[-1])], ftiles[:int(foff[-1])])
+        exp_t = ftiles[:int(foff[-1])].cpu().numpy().copy()
+        if world > 1:   # each union list: this rank's key blocks first, each group ascending
+            fo = foff.cpu().numpy()
+            for sl in range(2 * fp):
+                seg = exp_t[fo[sl]:fo[sl + 1]].tolist()
+                exp_t[fo[sl]:fo[sl + 1]] = ([e for e in seg if owner[e >> 2] == rank] +
+                                            [e for e in seg if owner[e >> 2] != rank])
+        assert at.fwd_slot_tiles[:int(foff[-1])].cpu().tolist() == exp_t.tolist()
         assert fsh_d.cpu().tolist() == [int(x) for x in fsh]
         n_pairs, n_rest = at.counts.cpu().tolist()
         # shared pairs heavy-first by union length, ties by pair index (fwd_pair_w), and
