@@ -228,7 +228,8 @@ typedef struct BamAttnBwdParams {
   const int32_t* pair_shared;
   int32_t n_slots, pad_;
   int32_t kv_head_major;    /* k/v head-major [Hkv, k_rows*128, 128] */
-  int32_t pad2_;
+  int32_t dkv_bf16;         /* != 0: dk / dv are bf16 [k_rows*128, Hkv, 128] (complete
+                               gradients, one GPU: no partial sums follow), else fp32 */
   /* Optional CP reduce-scatter fused into the epilogue: when dkv_peers != NULL
    * (a DEVICE array of one pointer per rank, each the UVA address of this
    * rank's slot [2][Hkv][dkv_rows_per_owner][128] fp32 in that rank's
@@ -349,6 +350,15 @@ int bam_reduce_partials_bf16(const float* src, int32_t n_parts, int64_t part_str
                              int64_t comp_stride, int64_t head_stride, int64_t row_stride,
                              int32_t n_heads, int64_t n_rows, void* dst0, void* dst1,
                              void* stream);
+
+/* Token-major K and V [n, nkv, 128] bf16 -> head-major [nkv, rows_i, 128] at
+ * rows [off_i, off_i + n) of destination 0 and, when k1 != NULL, destination 1,
+ * in one launch: this rank's shard into its symmetric buffer (pulled by the
+ * peers) and into its slot of the gathered K/V the CP forward reads.  Replaces
+ * four strided copies on the forward's critical path. */
+int bam_kv_head_major(const void* k, const void* v, int64_t n, int32_t nkv, void* k0, void* v0,
+                      int64_t rows0, int64_t off0, void* k1, void* v1, int64_t rows1,
+                      int64_t off1, void* stream);
 
 /* fp32 -> bf16 conversion (dk/dv partials to the bf16 gradient layout). */
 int bam_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);

@@ -57,7 +57,7 @@ class BamAttnBwdParams(ctypes.Structure):
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("pair_shared", c_vp), ("n_slots", c_i32), ("pad_", c_i32),
-                ("kv_head_major", c_i32), ("pad2_", c_i32),
+                ("kv_head_major", c_i32), ("dkv_bf16", c_i32),
                 ("dkv_peers", c_vp), ("dkv_rows_per_owner", c_i32), ("pad3_", c_i32)]
 
 
@@ -90,6 +90,8 @@ SIGNATURES = {
     "bam_reduce_partials_bf16": (c_i32, [c_vp, c_i32, c_i64, c_i64, c_i64, c_i64, c_i32, c_i64,
                                          c_vp, c_vp, c_vp]),
     "bam_permute_blocks": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "bam_kv_head_major": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+                                  c_i64, c_i64, c_vp]),
     "bam_stream_write_i32": (c_i32, [c_vp, c_i32, c_vp]),
     "bam_copy_2d": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp]),
     "bam_stream_wait_i32_geq": (c_i32, [c_vp, c_i32, c_vp]),
@@ -162,7 +164,8 @@ KERNELS_PER_CALL = {
     "bam_attn_fwd": 1, "bam_attn_bwd": 3, "bam_attn_bwd_preprocess": 1, "bam_attn_bwd_main": 1,
     "bam_attn_bwd_finalize": 1, "bam_f32_to_bf16": 1, "bam_selftest_umma": 1,
     "bam_reduce_partials_bf16": 1,
-    "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1, "bam_plan_build": 15,
+    "bam_build_pair_lists": 2, "bam_attn_fwd_combine": 1, "bam_plan_build": 19,
+    "bam_kv_head_major": 1,
     "bam_stream_write_i32": 0, "bam_stream_wait_i32_geq": 0,   # stream memory operations
     "bam_copy_2d": 0,                                         # copy engine
 }

@@ -349,7 +349,7 @@ class BackwardWorkspace:
         return self.plan.pair_shared is not None and os.environ.get("BAM_BWD_PAIRS", "1") != "0"
 
     def _params(self, k, v, dk, dv, h_begin, nh, Hkv, kv_head_major=False, dkv_peers=None,
-                rows_per_owner=0):
+                rows_per_owner=0, dkv_bf16=False):
         pl = self.plan
         pairs = self._pairs()
         col_off, col_tiles, order = ((pl.slot_off, pl.slot_tiles, pl.slot_kb) if pairs else
@@ -363,19 +363,20 @@ class BackwardWorkspace:
             col_tiles.data_ptr(), order.data_ptr(), pl.nq, pl.nb, pl.k_rows,
             self.q.shape[1], Hkv, self.scale, h_begin, nh,
             pl.pair_shared.data_ptr() if pairs else None,
-            int(pl.slot_kb.shape[0]) if pairs else 0, 0, int(kv_head_major), 0,
+            int(pl.slot_kb.shape[0]) if pairs else 0, 0, int(kv_head_major), int(dkv_bf16),
             dkv_peers.data_ptr() if dkv_peers is not None else None, int(rows_per_owner), 0)
 
     def _call(self, name, k, v, dk, dv, h_begin, nh, Hkv, **kw):
         _lib.call(name, self._params(k, v, dk, dv, h_begin, nh, Hkv, **kw))
 
     def main(self, k, v, *, h_begin=0, nh=0, timer=None, kv_head_major=False, dkv_peers=None,
-             rows_per_owner=0):
+             rows_per_owner=0, bf16=False):
         """dK/dV fp32 partials of the head group, [k_rows*128, Hkv, 128]; dQ
         accumulates.  kv_head_major: k/v are [Hkv, k_rows*128, 128].
         dkv_peers (int64 device tensor of per-rank workspace-slot addresses)
         with rows_per_owner: the partials go straight to their owners (fused
-        reduce-scatter); returns (None, None)."""
+        reduce-scatter); returns (None, None).  bf16: the kernel writes the
+        complete bf16 gradients (one GPU, no partial sums follow)."""
         rows = self.plan.k_rows * BLOCK
         if kv_head_major:
             Hkv = _check_kv_head_major(k, v, self.plan)
@@ -387,13 +388,14 @@ class BackwardWorkspace:
         if dkv_peers is not None:
             dk = dv = None
         else:
-            dk = torch.empty((rows, Hkv, HEAD_DIM), dtype=torch.float32, device=k.device)
-            dv = torch.empty((rows, Hkv, HEAD_DIM), dtype=torch.float32, device=k.device)
+            dt = torch.bfloat16 if bf16 else torch.float32
+            dk = torch.empty((rows, Hkv, HEAD_DIM), dtype=dt, device=k.device)
+            dv = torch.empty((rows, Hkv, HEAD_DIM), dtype=dt, device=k.device)
         if timer is not None:
             timer[0].record()
         self._call("bam_attn_bwd_main", k, v, dk, dv, h_begin, nh, Hkv,
                    kv_head_major=kv_head_major, dkv_peers=dkv_peers,
-                   rows_per_owner=rows_per_owner)
+                   rows_per_owner=rows_per_owner, dkv_bf16=bf16 and dkv_peers is None)
         if timer is not None:
             timer[1].record()
         return dk, dv
@@ -409,11 +411,8 @@ def attn_backward(q, k, v, o, lse, do, plan: AttentionPlan, scale: float | None 
     partials when ``dkv_fp32`` (for a CP reduce-scatter), else bf16."""
     _check_qkv(q, k, v, plan)
     ws = BackwardWorkspace(q, o, lse, do, plan, scale)
-    dk, dv = ws.main(k, v, timer=timer)
-    dq = ws.finalize()
-    if dkv_fp32:
-        return dq, dk, dv
-    return dq, to_bf16(dk), to_bf16(dv)
+    dk, dv = ws.main(k, v, timer=timer, bf16=not dkv_fp32)
+    return ws.finalize(), dk, dv
 
 
 def to_bf16(x: torch.Tensor) -> torch.Tensor:

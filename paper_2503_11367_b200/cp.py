@@ -232,13 +232,13 @@ class SymmExchange:
             chunks -= 1
         n = k_g.shape[0]
         mine = self.kv[:2 * rows * nkv * d].view(2, nkv, rows, d)
-        mine[0, :, :n].copy_(k_g.transpose(0, 1))
-        mine[1, :, :n].copy_(v_g.transpose(0, 1))
         k_all = torch.empty((nkv, self.world * rows, d), dtype=k_g.dtype, device=k_g.device)
         v_all = torch.empty_like(k_all)
-        lo = self.rank * rows
-        k_all[:, lo:lo + n].copy_(mine[0, :, :n])
-        v_all[:, lo:lo + n].copy_(mine[1, :, :n])
+        # this rank's rows, head-major, into its symmetric buffer and its gathered slot
+        kc, vc = k_g.contiguous(), v_g.contiguous()
+        _lib.call("bam_kv_head_major", kc.data_ptr(), vc.data_ptr(), n, nkv,
+                  mine[0].data_ptr(), mine[1].data_ptr(), rows, 0, k_all.data_ptr(),
+                  v_all.data_ptr(), self.world * rows, self.rank * rows)
         self.kv_h.barrier(channel=0)          # every rank's slice is in place
         cur = torch.cuda.current_stream()
         ev_local = torch.cuda.Event()
@@ -587,8 +587,8 @@ def cp_backward(q_loc, gathered, o, lse, do, plan: CPPlan, group=None, scale=Non
     ws = A.BackwardWorkspace(q_loc, o, lse, do, plan.attn, scale)
     if transport == "local":
         k_all, v_all = gathered[0]
-        dk, dv = ws.main(k_all, v_all, timer=None if timers is None else timers[0])
-        return ws.finalize(), A.to_bf16(dk), A.to_bf16(dv)
+        dk, dv = ws.main(k_all, v_all, timer=None if timers is None else timers[0], bf16=True)
+        return ws.finalize(), dk, dv
     cur = torch.cuda.current_stream()
     comm = _comm_stream(q_loc.device)
     rows = plan.layout.max_blocks * BLOCK

@@ -532,6 +532,23 @@ __global__ void __maxnreg__(128)
               : "memory");
         }
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      } else if (p.dkv_bf16) {
+        // one GPU: the complete gradient row, rounded to bf16 here (no fp32 round trip)
+        uint4* d16 = reinterpret_cast<uint4*>(
+            reinterpret_cast<__nv_bfloat16*>(c == 0 ? p.dv : p.dk) + (row * p.Hkv + hkv) * 128);
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          uint32_t a[32];
+          BAM_TMEM_LD32(tmem + lane_base + (c == 0 ? kColDV : kColDK) + q * 32, a);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            d16[q * 4 + i] = make_uint4(
+                pack_bf16(__uint_as_float(a[8 * i]) * mul, __uint_as_float(a[8 * i + 1]) * mul),
+                pack_bf16(__uint_as_float(a[8 * i + 2]) * mul, __uint_as_float(a[8 * i + 3]) * mul),
+                pack_bf16(__uint_as_float(a[8 * i + 4]) * mul, __uint_as_float(a[8 * i + 5]) * mul),
+                pack_bf16(__uint_as_float(a[8 * i + 6]) * mul, __uint_as_float(a[8 * i + 7]) * mul));
+        }
       } else
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
@@ -545,6 +562,10 @@ __global__ void __maxnreg__(128)
                               __uint_as_float(a[4 * i + 2]) * mul,
                               __uint_as_float(a[4 * i + 3]) * mul);
       }
+    } else if (p.dkv_bf16 && p.dkv_peers == nullptr) {
+      uint4* d16 = reinterpret_cast<uint4*>(
+          reinterpret_cast<__nv_bfloat16*>(c == 0 ? p.dv : p.dk) + (row * p.Hkv + hkv) * 128);
+      for (int i = 0; i < 16; ++i) d16[i] = make_uint4(0u, 0u, 0u, 0u);
     } else {
       float4* d4 = reinterpret_cast<float4*>(dst);
       for (int i = 0; i < 32; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -612,12 +633,13 @@ __global__ void __maxnreg__(128)
   BAM_CTA_CLOCK_END(nsteps);
 }
 
-// ld[h, 0, row] = lse[h, row] * log2e, ld[h, 1, row] = sum_d dO[row, h, d] * O[row, h, d]
-// (one warp per (row, h))
+// ld[h, 0, row] = lse[h, row] * log2e, ld[h, 1, row] = sum_d dO[row, h, d] * O[row, h, d],
+// and the dQ accumulator row dq_acc[h, row, :] = 0 (one warp per (row, h); the
+// zeroing replaces a separate 2-GB memset at config 4)
 __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
                                  const __nv_bfloat16* __restrict__ dout,
                                  const float* __restrict__ lse, int64_t rows, int H,
-                                 float* __restrict__ ld) {
+                                 float* __restrict__ ld, float* __restrict__ dq_acc) {
   // one warp per 4 (row, head) items: 8 independent 8-B loads in flight per lane
   const int64_t nw = rows * H;
   const int lane = lane_id();
@@ -629,6 +651,14 @@ __global__ void bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
       const int64_t w = w0 + u < nw ? w0 + u : nw - 1;
       a[u] = __ldcs(reinterpret_cast<const uint2*>(o + w * 128) + lane);
       b[u] = __ldcs(reinterpret_cast<const uint2*>(dout + w * 128) + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (w0 + u < nw) {
+        const int64_t w = w0 + u, row = w / H, h = w - row * H;
+        reinterpret_cast<float4*>(dq_acc + (h * rows + row) * 128)[lane] =
+            make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
     float acc[4];
 #pragma unroll
@@ -737,6 +767,7 @@ static int check_bwd(const BamAttnBwdParams* pp) {
                 "bam_attn_bwd: head group [%d, %d) of Hq=%d over Hkv=%d", p.h_begin,
                 p.h_begin + nh, p.Hq, p.Hkv);
   BAM_CHECK_ARG(p.nb <= 65535, "bam_attn_bwd: nb=%d > 65535", p.nb);
+  BAM_CHECK_ARG(!(p.dkv_bf16 && p.dkv_peers), "bam_attn_bwd: dkv_bf16 with dkv_peers");
   BAM_CHECK_ARG(p.dkv_peers == nullptr ||
                     (p.dkv_rows_per_owner >= 128 && p.dkv_rows_per_owner % 128 == 0 &&
                      (int64_t)p.k_rows * 128 % p.dkv_rows_per_owner == 0),
@@ -781,9 +812,8 @@ int bam_attn_bwd_preprocess(const BamAttnBwdParams* pp, void* stream) {
   const int64_t rows = (int64_t)p.nq * 128;
   bwd::bwd_delta_kernel<<<148 * 8, 256, 0, s>>>((const __nv_bfloat16*)p.o,
                                                 (const __nv_bfloat16*)p.dout, p.lse, rows, p.Hq,
-                                                p.delta);
+                                                p.delta, p.dq_acc);
   BAM_LAUNCH_CHECK();
-  BAM_CUDA_TRY(cudaMemsetAsync(p.dq_acc, 0, sizeof(float) * rows * p.Hq * 128, s));
   return kOk;
 }
 

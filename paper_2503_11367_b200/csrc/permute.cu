@@ -79,6 +79,28 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(
   }
 }
 
+// Token-major K/V [n, nkv, 128] bf16 -> head-major [nkv, rows_i, 128] at row
+// offset off_i of up to two destinations (the copy-engine CP gather: this rank's
+// shard into its symmetric buffer, which the peers pull, and into its own slot of
+// the gathered buffer the forward reads).  One 16-B vector per thread per
+// tensor: reads are contiguous, writes are 256-B runs per (token, head).
+__global__ void __launch_bounds__(256) kv_head_major_kernel(
+    const uint4* __restrict__ k, const uint4* __restrict__ v, int64_t n, int32_t nkv,
+    uint4* __restrict__ k0, uint4* __restrict__ v0, int64_t rows0, int64_t off0,
+    uint4* __restrict__ k1, uint4* __restrict__ v1, int64_t rows1, int64_t off1) {
+  const int64_t per = n * nkv * 16;   // vectors per tensor
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < 2 * per; e += stride) {
+    const bool is_v = e >= per;
+    const int64_t i = is_v ? e - per : e;
+    const uint4 x = __ldcs((is_v ? v : k) + i);
+    const int64_t c = i & 15, th = i >> 4;
+    const int64_t t = th / nkv, h = th - t * nkv;
+    (is_v ? v0 : k0)[((h * rows0) + off0 + t) * 16 + c] = x;
+    if (k1 != nullptr) (is_v ? v1 : k1)[((h * rows1) + off1 + t) * 16 + c] = x;
+  }
+}
+
 }  // namespace perm
 }  // namespace bam
 
@@ -129,6 +151,28 @@ extern "C" int bam_reduce_partials_bf16(const float* src, int32_t n_parts, int64
   perm::reduce_partials_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
       src, n_parts, part_stride, comp_stride, head_stride, row_stride, n_heads, n_rows,
       static_cast<uint4*>(dst0), static_cast<uint4*>(dst1), dst1 ? 2 : 1);
+  BAM_LAUNCH_CHECK();
+  return kOk;
+}
+
+extern "C" int bam_kv_head_major(const void* k, const void* v, int64_t n, int32_t nkv,
+                                 void* k0, void* v0, int64_t rows0, int64_t off0, void* k1,
+                                 void* v1, int64_t rows1, int64_t off1, void* stream) {
+  BAM_CHECK_ARG(n >= 0 && nkv >= 1, "bam_kv_head_major: n=%lld nkv=%d", (long long)n, nkv);
+  if (n == 0) return kOk;
+  BAM_CHECK_ARG(k && v && k0 && v0 && off0 >= 0 && off0 + n <= rows0 &&
+                    (k1 == nullptr || (v1 && off1 >= 0 && off1 + n <= rows1)),
+                "bam_kv_head_major: n=%lld nkv=%d rows0=%lld off0=%lld rows1=%lld off1=%lld",
+                (long long)n, nkv, (long long)rows0, (long long)off0, (long long)rows1,
+                (long long)off1);
+  BAM_CHECK_ARG(((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+                  reinterpret_cast<uintptr_t>(k0) | reinterpret_cast<uintptr_t>(v0) |
+                  reinterpret_cast<uintptr_t>(k1) | reinterpret_cast<uintptr_t>(v1)) & 15) == 0,
+                "bam_kv_head_major: pointers must be 16-byte aligned");
+  perm::kv_head_major_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint4*>(k), static_cast<const uint4*>(v), n, nkv,
+      static_cast<uint4*>(k0), static_cast<uint4*>(v0), rows0, off0, static_cast<uint4*>(k1),
+      static_cast<uint4*>(v1), rows1, off1);
   BAM_LAUNCH_CHECK();
   return kOk;
 }

@@ -353,6 +353,32 @@ def test_cp_emulated_world8_config4_overlapped_forward():
     assert rel_l2(dv_sum, dv_1) < 1e-2 and (dv_sum - dv_1).abs().max().item() < 2e-2
 
 
+def test_kv_head_major_bit_exact():
+    """bam_kv_head_major (the copy-engine gather's local step) against torch
+    transposes: both destinations, row offsets, one and two outputs."""
+    from paper_2503_11367_b200 import _lib
+
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(4)
+    for n, nkv in ((384, 8), (128, 3), (0, 2)):
+        k = torch.randn(n, nkv, 128, device=dev, generator=g).to(torch.bfloat16)
+        v = torch.randn(n, nkv, 128, device=dev, generator=g).to(torch.bfloat16)
+        r0, o0, r1, o1 = n + 256, 128, 4 * n + 128, 2 * n
+        k0 = torch.zeros(nkv, r0, 128, dtype=torch.bfloat16, device=dev)
+        v0, k1, v1 = torch.zeros_like(k0), torch.zeros(nkv, r1, 128, dtype=torch.bfloat16,
+                                                      device=dev), None
+        v1 = torch.zeros_like(k1)
+        _lib.call("bam_kv_head_major", k.data_ptr(), v.data_ptr(), n, nkv, k0.data_ptr(),
+                  v0.data_ptr(), r0, o0, k1.data_ptr(), v1.data_ptr(), r1, o1)
+        torch.cuda.synchronize()
+        for dst, src, off in ((k0, k, o0), (v0, v, o0), (k1, k, o1), (v1, v, o1)):
+            assert torch.equal(dst[:, off:off + n], src.transpose(0, 1))
+            assert dst[:, :off].abs().sum().item() == 0 and dst[:, off + n:].abs().sum().item() == 0
+    with pytest.raises(Exception, match="bam_kv_head_major"):
+        _lib.call("bam_kv_head_major", k0.data_ptr(), v0.data_ptr(), 10, 2, k0.data_ptr(),
+                  v0.data_ptr(), 5, 0, None, None, 0, 0)
+
+
 def test_cp_emulated_mha_overlapped_forward():
     """MHA under the overlapped copy-engine forward: the query-block-pair kernel's
     union lists are local-first (bam_plan_build), so its CTAs start on this rank's
