@@ -360,3 +360,41 @@ def test_fwd_class_order_matches_head_pair_major():
                 os.environ["BAM_FWD_CLASS_ORDER"] = old
         torch.cuda.synchronize()
         assert torch.equal(o0, o1) and torch.equal(l0, l1), (Hq, Hkv)
+
+
+def test_bwd_cta_pairs_match_single_ctas():
+    """Backward CTA pairs (clusters of 2 multicasting Q/dO over union step lists,
+    class 0 where a key block does not see the query block) against one CTA per
+    key block (BAM_BWD_PAIRS=0): dK / dV bit-identical (a class-0 step adds exact
+    zeros, the step order per key block is the same), dQ within fp32 reduction
+    order."""
+    import os
+    from paper_2503_11367_b200 import attention as A, mask as M
+    from paper_2503_11367_b200.workloads import emu_interleave
+
+    mask = M.build_bitfield(emu_interleave(8 * 1024, seed=5))
+    plan = A.plan_for_mask(mask)
+    assert int(plan.pair_shared.sum()) > 0
+    T, Hq, Hkv = len(mask), 4, 2
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(8)
+    q, do = (torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+             for _ in range(2))
+    k, v = (torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+            for _ in range(2))
+    o, lse = A.attn_forward(q, k, v, plan)
+    out = {}
+    old = os.environ.get("BAM_BWD_PAIRS")
+    try:
+        for mode in ("1", "0"):
+            os.environ["BAM_BWD_PAIRS"] = mode
+            out[mode] = A.attn_backward(q, k, v, o, lse, do, plan, dkv_fp32=True)
+    finally:
+        if old is None:
+            os.environ.pop("BAM_BWD_PAIRS", None)
+        else:
+            os.environ["BAM_BWD_PAIRS"] = old
+    torch.cuda.synchronize()
+    (dq1, dk1, dv1), (dq0, dk0, dv0) = out["1"], out["0"]
+    assert torch.equal(dk1, dk0) and torch.equal(dv1, dv0)
+    assert rel_l2(dq1, dq0) < 1e-3
