@@ -186,7 +186,7 @@ class SymmExchange:
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
         self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
-        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "8"))
+        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "2"))   # pull streams
         self._cache = {}
 
     def _check(self, rows: int, kv0: int, nkv: int):
@@ -217,12 +217,16 @@ class SymmExchange:
                           head_chunks: int | None = None):
         """K/V all-gather that lets the attention start early, into HEAD-MAJOR
         buffers [nkv, world*rows, d]: this rank's rows go straight into the
-        gathered buffers before the barrier (event ``ev_local``); the peers'
-        shards are pulled in ``head_chunks`` groups of KV heads per peer (one
-        strided copy-engine copy per (peer, group, K|V), ``bam_copy_2d``), each
-        followed by stream-ordered flag stores ``flags[peer*nkv + h] = epoch``
-        (bam_stream_write_i32, no SM) that the forward kernel waits on per
-        tile, so the first heads' tiles start after a fraction of the transfer.
+        gathered buffers before the barrier (event ``ev_local``, one
+        ``bam_kv_head_major`` launch); the peers' shards are then pulled PEER BY
+        PEER in rotation order rank+1, rank+2, ... (the order of the forward's
+        tile lists, bam_plan_build), on ``head_chunks`` copy streams that each
+        own a group of KV heads: per (peer, group, K|V) one strided copy-engine
+        copy (``bam_copy_2d``) followed by stream-ordered flag stores
+        ``flags[peer*nkv + h] = epoch`` (bam_stream_write_i32, no SM) that the
+        forward kernel waits on per tile.  Every rank pulls from a different peer
+        at a time; two streams measured 557 GB/s per rank at N=4 (per-head copies
+        from all peers at once: 300-367, tools/exchange_bw.py).
         ``ev_all``: every pull landed.
         Returns (k_all, v_all, ev_local, ev_all, (flags, epoch))."""
         nkv, d = k_g.shape[1], self.d
@@ -251,11 +255,12 @@ class SymmExchange:
         row_b = rows * d * 2                   # one head's rows of one rank, bytes
         dpitch = self.world * row_b
 
-        def pull(r):
+        def pull_group(g):
             def fn():
-                src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, 0)
-                for g in range(chunks):
-                    h0 = g * per
+                h0 = g * per
+                for step in range(1, self.world):
+                    r = (self.rank + step) % self.world
+                    src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, 0)
                     for t, dst in ((0, k_all), (1, v_all)):
                         _lib.call("bam_copy_2d", dst[h0, r * rows:].data_ptr(), dpitch,
                                   src[t, h0].data_ptr(), row_b, row_b, per)
@@ -263,7 +268,7 @@ class SymmExchange:
                         _lib.call("bam_stream_write_i32", self.flags[r * nkv + h:].data_ptr(),
                                   epoch)
             return fn
-        self._fan_out([pull((self.rank + step) % self.world) for step in range(1, self.world)])
+        self._fan_out([pull_group(g) for g in range(chunks)])
         for t in (k_all, v_all):
             for st in self.streams:
                 t.record_stream(st)
@@ -518,8 +523,9 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
     ex = plan.exchange(Hkv, d, k_loc.device, group) if transport == "ce" else None
     if ex is not None and len(hg) == 1:
         # the forward starts on this rank's key tiles while the copy engines pull the
-        # peers' K/V: every tile list is local-first (CSR rows and, for MHA, the
-        # query-block pairs' union lists), so no CTA waits before its local tiles
+        # peers' K/V: every tile list (CSR rows and, for MHA, the query-block pairs'
+        # union lists) holds this rank's key blocks first, then each peer's in the
+        # order the pulls land
         comm.wait_stream(cur)
         with torch.cuda.stream(comm):
             k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(

@@ -17,7 +17,8 @@ __global__ void list_fill_rows_kernel(const uint8_t* __restrict__ classes, int64
                                       const int32_t* __restrict__ q_gid,
                                       const int32_t* __restrict__ row_off,
                                       int32_t* __restrict__ row_tiles,
-                                      const int32_t* __restrict__ owner, int32_t rank);
+                                      const int32_t* __restrict__ owner, int32_t rank,
+                                      int32_t world);
 __global__ void list_fill_cols_kernel(const uint8_t* __restrict__ classes, int64_t nb,
                                       const int32_t* __restrict__ q_gid, int32_t nq,
                                       const int32_t* __restrict__ col_off,

@@ -218,7 +218,8 @@ __global__ void list_fill_rows_kernel(const uint8_t* __restrict__ classes, int64
                                       const int32_t* __restrict__ q_gid,
                                       const int32_t* __restrict__ row_off,
                                       int32_t* __restrict__ row_tiles,
-                                      const int32_t* __restrict__ owner, int32_t rank) {
+                                      const int32_t* __restrict__ owner, int32_t rank,
+                                      int32_t world) {
   __shared__ int warp_tot[32];
   __shared__ int carry;
   const int j = blockIdx.x;
@@ -226,11 +227,14 @@ __global__ void list_fill_rows_kernel(const uint8_t* __restrict__ classes, int64
   int32_t* out = row_tiles + row_off[j];
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int pass = 0; pass < (owner ? 2 : 1); ++pass) {
+  // under CP: the owners in rotation order rank, rank+1, ... (this rank's key
+  // blocks first, then the peers in the order the copy engines pull them)
+  for (int pass = 0; pass < (owner ? world : 1); ++pass) {
+    const int want = (rank + pass) % (world > 0 ? world : 1);
     for (int64_t base = 0; base < nb; base += blockDim.x) {
       const int64_t kb = base + threadIdx.x;
       int cls = kb < nb ? r[kb] : 0;
-      if (owner && cls && ((owner[kb] == rank) != (pass == 0))) cls = 0;
+      if (owner && cls && owner[kb] != want) cls = 0;
       const uint32_t m = __ballot_sync(0xffffffffu, cls != 0);
       if (lane_id() == 0) warp_tot[threadIdx.x >> 5] = __popc(m);
       __syncthreads();
@@ -383,7 +387,8 @@ int bam_build_tile_lists(const uint8_t* classes, int64_t nb, const int32_t* q_gi
   scan_kernel<<<1, 1024, 0, s>>>(col_cnt, nb, col_off);
   BAM_LAUNCH_CHECK();
   if (row_tiles) {
-    list_fill_rows_kernel<<<nq, 256, 0, s>>>(classes, nb, q_gid, row_off, row_tiles, nullptr, 0);
+    list_fill_rows_kernel<<<nq, 256, 0, s>>>(classes, nb, q_gid, row_off, row_tiles, nullptr, 0,
+                                             1);
     BAM_LAUNCH_CHECK();
   }
   if (col_tiles) {

@@ -125,8 +125,9 @@ __global__ void __launch_bounds__(1024) fwd_pairs_kernel(const int32_t* __restri
 // (element e -> classes[q_gid[e]][list]); else query-block rows over the key
 // blocks (classes[q_gid[list]][e]).  Pass 1 (tiles == nullptr) counts: a pair
 // is shared when its union is at most 9/8 of the longer list; pass 2 fills,
-// ascending -- for rows under CP (owner != NULL) this rank's key blocks first,
-// like the CSR rows, so the forward can start before the peers' K/V land.
+// ascending -- for rows under CP (owner != NULL) grouped by owner in the CSR
+// rows' rotation order (this rank's key blocks first, then rank+1, ...), so the
+// forward can start before the peers' K/V land.
 template <bool kCols>
 __global__ void __launch_bounds__(256) pair_lists_dense_kernel(
     const uint8_t* __restrict__ classes, int32_t nb, const int32_t* __restrict__ q_gid,
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(256) pair_lists_dense_kernel(
     int32_t* __restrict__ slot_kb, int32_t* __restrict__ slot_cnt,
     const int32_t* __restrict__ slot_off, int32_t* __restrict__ tiles,
     int32_t* __restrict__ pair_shared, const int32_t* __restrict__ owner = nullptr,
-    int32_t rank = 0) {
+    int32_t rank = 0, int32_t world = 1) {
   __shared__ int wa[8], wb[8], wu[8];
   __shared__ int carry_a, carry_b;
   const int pr = blockIdx.x;
@@ -187,12 +188,12 @@ __global__ void __launch_bounds__(256) pair_lists_dense_kernel(
   int32_t* ob = tiles + slot_off[2 * pr + 1];
   if (threadIdx.x == 0) carry_a = carry_b = 0;
   __syncthreads();
-  const bool local_first = !kCols && owner != nullptr;
-  for (int pass = 0; pass < (local_first ? 2 : 1); ++pass)
+  const bool by_owner = !kCols && owner != nullptr;
+  for (int pass = 0; pass < (by_owner ? world : 1); ++pass)
   for (int base = 0; base < n_elem; base += 256) {
     const int e = base + threadIdx.x;
     int ca = cls(ra, e), cb = cls(rb, e);
-    if (local_first && e < n_elem && ((owner[e] == rank) != (pass == 0))) ca = cb = 0;
+    if (by_owner && e < n_elem && owner[e] != (rank + pass) % world) ca = cb = 0;
     // shared: both slots walk the union (class 0 where a list lacks the element)
     const bool ka = sh ? (ca | cb) != 0 : ca != 0, kb2 = sh ? ka : cb != 0;
     const uint32_t ma = __ballot_sync(0xffffffffu, ka), mb = __ballot_sync(0xffffffffu, kb2);
@@ -306,10 +307,11 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
   list_count_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.row_cnt, p.col_cnt);
   scan_kernel<<<1, 1024, 0, s>>>(p.row_cnt, nq, p.row_off);
   scan_kernel<<<1, 1024, 0, s>>>(p.col_cnt, nb, p.col_off);
-  // rows: this rank's key blocks first under CP (the forward works on local K/V
-  // while the peers' rows are still arriving), each group ascending
+  // rows: under CP this rank's key blocks first, then each peer's in the order
+  // rank+1, rank+2, ... that the copy engines pull them (the forward works on local
+  // K/V while the peers' rows are still arriving), each group ascending
   list_fill_rows_kernel<<<nq, 256, 0, s>>>(p.classes, nb, p.q_gid, p.row_off, p.row_tiles,
-                                           p.world > 1 ? p.owner : nullptr, p.rank);
+                                           p.world > 1 ? p.owner : nullptr, p.rank, p.world);
   list_fill_cols_kernel<<<nb, 256, 0, s>>>(p.classes, nb, p.q_gid, nq, p.col_off, p.col_tiles);
   BAM_LAUNCH_CHECK();
   // heavy-first orders (LPT's sort key: -count, then index)
@@ -332,7 +334,8 @@ extern "C" int bam_plan_build(const BamPlan* pp, void* stream) {
   pair_lists_dense_kernel<false><<<fp, 256, 0, s>>>(p.classes, nb, p.q_gid, nb, p.fwd_order, nq,
                                                     p.fwd_slot_q, p.fwd_slot_cnt, p.fwd_slot_off,
                                                     p.fwd_slot_tiles, p.fwd_shared,
-                                                    p.world > 1 ? p.owner : nullptr, p.rank);
+                                                    p.world > 1 ? p.owner : nullptr, p.rank,
+                                                    p.world);
   fwd_pairs_kernel<<<1, 1024, 0, s>>>(p.fwd_shared, p.fwd_slot_q, p.row_cnt, fp, p.fwd_pair_ids,
                                       reinterpret_cast<int4*>(p.fwd_rest_items), p.counts);
   // shared pairs heavy-first by union length (the others weigh 0 and sort last, so

@@ -456,8 +456,8 @@ def test_cp_emulated_mha_overlapped_forward():
 def test_native_planner_matches_host_statement(policy, world):
     """bam_plan_build (one launch sequence, no host sync) against a host
     restatement with torch/Python of every list it builds: the gathered
-    layout (cp.cp_layout), CSR rows (ascending, and this rank's key blocks
-    first under CP), CSC columns, heavy-first orders (stable sort by -count),
+    layout (cp.cp_layout), CSR rows (ascending; under CP grouped by owner in
+    rotation order, this rank's key blocks first), CSC columns, heavy-first orders (stable sort by -count),
     the CTA-pair step lists (bam_build_pair_lists) and the forward pair /
     whole-row item compaction with its device counts."""
     from paper_2503_11367_b200 import _lib
@@ -486,9 +486,9 @@ def test_native_planner_matches_host_statement(policy, world):
         for j, b in enumerate(q_gid):
             kbs = np.nonzero(cls[b])[0]
             exp = [(kb << 2) | cls[b, kb] for kb in kbs]
-            if world > 1:   # this rank's key blocks first, each group ascending
-                exp = ([e for e in exp if owner[e >> 2] == rank] +
-                       [e for e in exp if owner[e >> 2] != rank])
+            if world > 1:   # owners in rotation order rank, rank+1, ..., each ascending
+                exp = [e for g in range(world) for e in exp
+                       if owner[e >> 2] == (rank + g) % world]
             assert rows[row_off[j]:row_off[j + 1]].tolist() == exp
         col_off = at.col_off.cpu().numpy()
         cols = at.col_tiles.cpu().numpy()
@@ -546,12 +546,12 @@ def test_native_planner_matches_host_statement(policy, world):
                   ftiles.data_ptr(), fsh_d.data_ptr())
         assert torch.equal(at.fwd_slot_q, fq) and torch.equal(at.fwd_slot_off, foff)
         exp_t = ftiles[:int(foff[-1])].cpu().numpy().copy()
-        if world > 1:   # each union list: this rank's key blocks first, each group ascending
+        if world > 1:   # each union list: owners in rotation order rank, rank+1, ...
             fo = foff.cpu().numpy()
             for sl in range(2 * fp):
                 seg = exp_t[fo[sl]:fo[sl + 1]].tolist()
-                exp_t[fo[sl]:fo[sl + 1]] = ([e for e in seg if owner[e >> 2] == rank] +
-                                            [e for e in seg if owner[e >> 2] != rank])
+                exp_t[fo[sl]:fo[sl + 1]] = [e for g in range(world) for e in seg
+                                            if owner[e >> 2] == (rank + g) % world]
         assert at.fwd_slot_tiles[:int(foff[-1])].cpu().tolist() == exp_t.tolist()
         assert fsh_d.cpu().tolist() == [int(x) for x in fsh]
         n_pairs, n_rest = at.counts.cpu().tolist()

@@ -7,8 +7,10 @@ Times, on the current stream with CUDA events (max over ranks), the forward
 K/V all-gather and the backward dK/dV reduce-scatter of the padded config-4
 shards, through both transports: "nccl" (cp.gather_kv / cp.scatter_dkv) and
 "ce" (cp.SymmExchange copy-engine pulls / pushes over torch symmetric
-memory, its device barriers included), plus "ce_head_major" = the
-gather_overlapped() pulls bench.py uses (one copy stream per peer).  Prints one JSON line per
+memory, its device barriers included), plus "ce_overlapped_<k>streams" = the
+gather_overlapped() pulls bench.py uses (peer by peer in rotation order on k
+streams, one group of KV heads each; k = 2 by default) and
+"ce_peer_sequential_<k>" (the same with a join between peers).  Prints one JSON line per
 (step, transport): peer bytes per rank (what crosses NVLink into, for the
 gather, or out of, for the reduce-scatter, one GPU) and that over the time.
 """
@@ -51,16 +53,68 @@ rs_bytes = (world - 1) * rows * Hkv * D * 4 * 2              # fp32 dK and dV to
 steps = {
     ("kv_all_gather", "nccl"): (lambda: cp.gather_kv(k_loc, v_loc, lay), gather_bytes),
     ("kv_all_gather", "ce"): (lambda: ex.gather(rows, 0, k_loc, v_loc), gather_bytes),
-    ("kv_all_gather", "ce_head_major"): (lambda: ex.gather_overlapped(rows, k_loc, v_loc, 8),
-                                         gather_bytes),
-    ("kv_all_gather", "ce_head_major_2chunks"): (
-        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 2), gather_bytes),
-    ("kv_all_gather", "ce_head_major_1chunk"): (
+    ("kv_all_gather", "ce_overlapped_2streams"): (
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 2), gather_bytes),   # bench.py's
+    ("kv_all_gather", "ce_overlapped_1stream"): (
         lambda: ex.gather_overlapped(rows, k_loc, v_loc, 1), gather_bytes),
+    ("kv_all_gather", "ce_overlapped_4streams"): (
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 4), gather_bytes),
+    ("kv_all_gather", "ce_overlapped_8streams"): (
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 8), gather_bytes),
+    ("kv_all_gather", "ce_peer_sequential_8"): (lambda: peer_sequential(rows, k_loc, v_loc, 8),
+                                                gather_bytes),
+    ("kv_all_gather", "ce_peer_sequential_4"): (lambda: peer_sequential(rows, k_loc, v_loc, 4),
+                                                gather_bytes),
+    ("kv_all_gather", "ce_peer_sequential_2"): (lambda: peer_sequential(rows, k_loc, v_loc, 2),
+                                                gather_bytes),
     ("dkv_reduce_scatter", "nccl"): (lambda: cp.scatter_dkv(dk_all, dv_all, lay), rs_bytes),
     ("dkv_reduce_scatter", "ce"): (lambda: ex.reduce_scatter(rows, 0, dk_all, dv_all, n_loc),
                                    rs_bytes),
 }
+
+
+def peer_sequential(rows, k_g, v_g, streams_per_peer):
+    """K/V gather into head-major buffers peer by peer (rotation order rank+1,
+    rank+2, ...): each peer's rows are pulled as ``streams_per_peer`` concurrent
+    head-group copies, the next peer starts when they are done (the arrival
+    pattern a row list sorted by owner would want, tools/fwd_order_sim.py)."""
+    from paper_2503_11367_b200 import _lib
+    nkv, d = k_g.shape[1], 128
+    n = k_g.shape[0]
+    mine = ex.kv[:2 * rows * nkv * d].view(2, nkv, rows, d)
+    k_all = torch.empty((nkv, world * rows, d), dtype=k_g.dtype, device=dev)
+    v_all = torch.empty_like(k_all)
+    _lib.call("bam_kv_head_major", k_g.data_ptr(), v_g.data_ptr(), n, nkv, mine[0].data_ptr(),
+              mine[1].data_ptr(), rows, 0, k_all.data_ptr(), v_all.data_ptr(), world * rows,
+              rank * rows)
+    ex.kv_h.barrier(channel=0)
+    cur = torch.cuda.current_stream()
+    while len(ex.streams) < streams_per_peer:
+        ex.streams.append(torch.cuda.Stream(device=dev))
+    per = nkv // streams_per_peer
+    row_b = rows * d * 2
+    prev = torch.cuda.Event()
+    prev.record(cur)
+    for step in range(1, world):
+        r = (rank + step) % world
+        src = ex.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, 0)
+        done = []
+        for i in range(streams_per_peer):
+            st = ex.streams[i]
+            st.wait_event(prev)
+            with torch.cuda.stream(st):
+                for t, dst in ((0, k_all), (1, v_all)):
+                    _lib.call("bam_copy_2d", dst[i * per, r * rows:].data_ptr(), world * row_b,
+                              src[t, i * per].data_ptr(), row_b, row_b, per)
+            e = torch.cuda.Event()
+            e.record(st)
+            done.append(e)
+        for e in done:
+            cur.wait_event(e)
+        prev = torch.cuda.Event()
+        prev.record(cur)
+    ex.kv_h.barrier(channel=0)
+    return k_all, v_all
 
 
 def sync():
