@@ -113,15 +113,22 @@ __device__ __forceinline__ uint4 bias_chunk(float x) {
 // P = 2^(S c - lse) for a pair of queries (packed FMUL2, exponentials on MUFU:
 // the backward's MUFU is ~25% busy, a polynomial share measured slower), masked by
 // the PARTIAL-tile allow bits.  The S columns already hold S - lse / c (bias MMA).
+template <bool kMasked>
 __device__ __forceinline__ float2 p_pair(uint32_t s0, uint32_t s1, float sc, int i2,
                                          uint32_t allow) {
   const float2 x = fmul2(make_float2(__uint_as_float(s0), __uint_as_float(s1)),
                          make_float2(sc, sc));
   float2 p = make_float2(ex2(x.x), ex2(x.y));
-  p.x = (allow >> (2 * i2)) & 1 ? p.x : 0.f;
-  p.y = (allow >> (2 * i2 + 1)) & 1 ? p.y : 0.f;
+  if constexpr (kMasked) {
+    p.x = (allow >> (2 * i2)) & 1 ? p.x : 0.f;
+    p.y = (allow >> (2 * i2 + 1)) & 1 ? p.y : 0.f;
+  }
   return p;
 }
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
 // dS = P (dP - D) for the same pair (the dP columns hold dP - D: bias MMA)
 __device__ __forceinline__ float2 ds_pair(float2 p, uint32_t dp0, uint32_t dp1) {
   return fmul2(p, make_float2(__uint_as_float(dp0), __uint_as_float(dp1)));
@@ -431,26 +438,34 @@ __global__ void __maxnreg__(128)
       }
       tmem_wait_ld();
       // P^T over this warpgroup's own S columns, released in kBwdPChunks chunks
+      // (FULL tiles -- nearly all of them -- skip the per-element allow test)
+      auto p_chunks = [&](auto masked) {
 #pragma unroll
-      for (int j = 0; j < kBwdPChunks; ++j) {
-        constexpr int kPer = 16 / kBwdPChunks;
-        uint32_t pk[kPer];
+        for (int j = 0; j < kBwdPChunks; ++j) {
+          constexpr int kPer = 16 / kBwdPChunks;
+          uint32_t pk[kPer];
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int i2 = j * kPer + u;
-          const float2 pp = p_pair(sr[2 * i2], sr[2 * i2 + 1], scale_log2, i2, allow);
-          sr[2 * i2] = __float_as_uint(pp.x);
-          sr[2 * i2 + 1] = __float_as_uint(pp.y);
-          pk[u] = pack_bf16(pp.x, pp.y);
+          for (int u = 0; u < kPer; ++u) {
+            const int i2 = j * kPer + u;
+            const float2 pp = p_pair<decltype(masked)::value>(sr[2 * i2], sr[2 * i2 + 1],
+                                                              scale_log2, i2, allow);
+            sr[2 * i2] = __float_as_uint(pp.x);
+            sr[2 * i2 + 1] = __float_as_uint(pp.y);
+            pk[u] = pack_bf16(pp.x, pp.y);
+          }
+          if constexpr (kPer == 16)
+            BAM_TMEM_ST16(tS + c * 32, pk);
+          else
+            BAM_TMEM_ST8(tS + c * 32 + j * 8, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&sm.bar_p_ready[j]);
         }
-        if constexpr (kPer == 16)
-          BAM_TMEM_ST16(tS + c * 32, pk);
-        else
-          BAM_TMEM_ST8(tS + c * 32 + j * 8, pk);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&sm.bar_p_ready[j]);
-      }
+      };
+      if (si.cls == 1)
+        p_chunks(BoolC<false>{});
+      else
+        p_chunks(BoolC<true>{});
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 5, s);
       mbar_wait_sleep<BAM_COMPUTE_SLEEP_NS>(&sm.bar_dp_full, ph);
       BAM_TRACE_EV(trace_cta && threadIdx.x == 0, 6, s);
