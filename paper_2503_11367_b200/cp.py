@@ -186,7 +186,7 @@ class SymmExchange:
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
         self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
-        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "2"))   # pull streams
+        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "1"))   # pull streams
         self._cache = {}
 
     def _check(self, rows: int, kv0: int, nkv: int):
@@ -225,8 +225,9 @@ class SymmExchange:
         copy (``bam_copy_2d``) followed by stream-ordered flag stores
         ``flags[peer*nkv + h] = epoch`` (bam_stream_write_i32, no SM) that the
         forward kernel waits on per tile.  Every rank pulls from a different peer
-        at a time; two streams measured 557 GB/s per rank at N=4 (per-head copies
-        from all peers at once: 300-367, tools/exchange_bw.py).
+        at a time; one stream (the default) measured 533-535 GB/s per rank at N=4,
+        two 482-520 (per-head copies from all peers at once: 300-367,
+        tools/exchange_bw.py).
         ``ev_all``: every pull landed.
         Returns (k_all, v_all, ev_local, ev_all, (flags, epoch))."""
         nkv, d = k_g.shape[1], self.d
