@@ -160,7 +160,9 @@ typedef struct BamAttnFwdParams {
   float* part_o;
   float* part_ml;
   int32_t n_items;
-  int32_t pad_;
+  int32_t kv_flag_heads;    /* head-major kv_ready: one flag per group of this many KV
+                               heads, kv_ready[g*Hkv + (h / kv_flag_heads) * kv_flag_heads]
+                               (0 or 1: one flag per (rank, KV head)) */
   /* Optional CP overlap (GQA head-pair kernel): kv_ready[g] >= kv_epoch once
    * rank g's K/V rows (block-rows [g*kv_rows_per_rank, (g+1)*kv_rows_per_rank)
    * of k/v) have landed; tiles of other ranks wait for it, this rank's

@@ -31,7 +31,8 @@ class BamAttnFwdParams(ctypes.Structure):
                 ("nq", c_i32), ("nb", c_i32), ("k_rows", c_i32), ("Hq", c_i32), ("Hkv", c_i32),
                 ("scale", c_f32), ("h_begin", c_i32), ("nh", c_i32),
                 ("items", c_vp), ("part_o", c_vp), ("part_ml", c_vp), ("n_items", c_i32),
-                ("pad_", c_i32), ("kv_ready", c_vp), ("kv_epoch", c_i32), ("kv_rank", c_i32),
+                ("kv_flag_heads", c_i32), ("kv_ready", c_vp), ("kv_epoch", c_i32),
+                ("kv_rank", c_i32),
                 ("kv_rows_per_rank", c_i32), ("kv_head_major", c_i32), ("dev_counts", c_vp),
                 ("order_classes", c_vp)]
 

@@ -232,12 +232,14 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
     after the last kernel launch (kernel-only time).
 
     ``kv_head_major``: k/v are [Hkv, k_rows*128, 128] instead of token-major
-    (then ``kv_ready`` flags are per (rank, KV head): ``flags[owner*Hkv + hkv]``).
+    (then ``kv_ready`` flags are per (rank, group of ``flag_heads`` KV heads):
+    ``flags[owner*Hkv + (hkv // flag_heads) * flag_heads]``).
 
-    ``kv_ready=(flags, epoch, rank, rows_per_rank)`` (context parallelism with
-    the copy-engine exchange): k/v may still be arriving; the GQA head-pair
-    kernel waits per tile until ``flags[owner] >= epoch`` for tiles of other
-    ranks (owner = block-row // rows_per_rank) and starts on this rank's own.
+    ``kv_ready=(flags, epoch, rank, rows_per_rank[, flag_heads])`` (context
+    parallelism with the copy-engine exchange): k/v may still be arriving; the
+    forward kernels wait per tile until the flag of its owner (block-row //
+    rows_per_rank) is >= epoch for tiles of other ranks and start on this
+    rank's own.
 
     Head groups (context-parallel pipelining): with ``nh`` > 0 only query
     heads [h_begin, h_begin+nh) are computed, against the ``k.shape[1]`` KV
@@ -284,11 +286,12 @@ def attn_forward(q, k, v, plan: AttentionPlan, scale: float | None = None, *,
         # CTA-pair kernel, nor split-KV schedules)
         if schedule is not None:
             raise ValueError("kv_ready needs whole rows")
-        flags, epoch, rank, rows_per_rank = kv_ready
+        flags, epoch, rank, rows_per_rank, *flag_heads = kv_ready
         if rows_per_rank < 1 or plan.k_rows // rows_per_rank > 64 or not 0 <= rank < 64:
             raise ValueError("kv_ready: rows_per_rank >= 1, at most 64 ranks")
         p.kv_ready, p.kv_epoch, p.kv_rank, p.kv_rows_per_rank = (flags.data_ptr(), int(epoch),
                                                                  int(rank), int(rows_per_rank))
+        p.kv_flag_heads = int(flag_heads[0]) if flag_heads else 0
     if timer is not None:
         timer[0].record()
     _launch_fwd(p, plan, schedule, (nh // Hkv) % 2 == 0, kv_ready is not None)

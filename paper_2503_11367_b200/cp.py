@@ -186,7 +186,7 @@ class SymmExchange:
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
         self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
-        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "1"))   # pull streams
+        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "2"))   # pull streams
         self._cache = {}
 
     def _check(self, rows: int, kv0: int, nkv: int):
@@ -222,14 +222,15 @@ class SymmExchange:
         PEER in rotation order rank+1, rank+2, ... (the order of the forward's
         tile lists, bam_plan_build), on ``head_chunks`` copy streams that each
         own a group of KV heads: per (peer, group, K|V) one strided copy-engine
-        copy (``bam_copy_2d``) followed by stream-ordered flag stores
-        ``flags[peer*nkv + h] = epoch`` (bam_stream_write_i32, no SM) that the
-        forward kernel waits on per tile.  Every rank pulls from a different peer
-        at a time; one stream (the default) measured 533-535 GB/s per rank at N=4,
-        two 482-520 (per-head copies from all peers at once: 300-367,
-        tools/exchange_bw.py).
+        copy (``bam_copy_2d``) followed by one stream-ordered flag store per
+        (peer, group) ``flags[peer*nkv + h0] = epoch`` (bam_stream_write_i32, no
+        SM; ``kv_flag_heads`` = the group size) that the forward kernel waits on
+        per tile.  Every rank pulls from a different peer
+        at a time; two streams joined per peer (the default) measured 556-560 GB/s
+        per rank at N=4, one stream 525-535 (per-head copies from all peers at
+        once: 300-367, tools/exchange_bw.py).
         ``ev_all``: every pull landed.
-        Returns (k_all, v_all, ev_local, ev_all, (flags, epoch))."""
+        Returns (k_all, v_all, ev_local, ev_all, (flags, epoch, heads per flag))."""
         nkv, d = k_g.shape[1], self.d
         self._check(rows, 0, nkv)
         chunks = max(1, min(nkv, head_chunks or self.head_chunks))
@@ -256,27 +257,45 @@ class SymmExchange:
         row_b = rows * d * 2                   # one head's rows of one rank, bytes
         dpitch = self.world * row_b
 
-        def pull_group(g):
-            def fn():
+        # peer by peer: the `chunks` streams pull one peer's head groups together and
+        # join before the next peer (without the join they drift onto different peers
+        # and measured 482-520 instead of 556-560 GB/s per rank at N=4 on two streams)
+        while len(self.streams) < chunks:
+            self.streams.append(torch.cuda.Stream(device=cur.device))
+        prev = torch.cuda.Event()
+        prev.record(cur)
+        for step in range(1, self.world):
+            r = (self.rank + step) % self.world
+            src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, 0)
+            done = []
+            for g in range(chunks):
+                st = self.streams[g]
+                st.wait_event(prev)
                 h0 = g * per
-                for step in range(1, self.world):
-                    r = (self.rank + step) % self.world
-                    src = self.kv_h.get_buffer(r, (2, nkv, rows, d), torch.bfloat16, 0)
+                with torch.cuda.stream(st):
                     for t, dst in ((0, k_all), (1, v_all)):
                         _lib.call("bam_copy_2d", dst[h0, r * rows:].data_ptr(), dpitch,
                                   src[t, h0].data_ptr(), row_b, row_b, per)
-                    for h in range(h0, h0 + per):
-                        _lib.call("bam_stream_write_i32", self.flags[r * nkv + h:].data_ptr(),
-                                  epoch)
-            return fn
-        self._fan_out([pull_group(g) for g in range(chunks)])
+                    # one flag per (peer, head group): BamAttnFwdParams.kv_flag_heads = per
+                    _lib.call("bam_stream_write_i32", self.flags[r * nkv + h0:].data_ptr(), epoch)
+                e = torch.cuda.Event()
+                e.record(st)
+                done.append(e)
+            if chunks == 1:
+                prev = done[0]
+            else:
+                prev = torch.cuda.Event()
+                for e in done:
+                    self.streams[0].wait_event(e)
+                prev.record(self.streams[0])
+        cur.wait_event(prev)
         for t in (k_all, v_all):
-            for st in self.streams:
+            for st in self.streams[:chunks]:
                 t.record_stream(st)
         ev_all = torch.cuda.Event()
         ev_all.record(cur)
         self.kv_h.barrier(channel=0)          # all pulls done before anyone rewrites
-        return k_all, v_all, ev_local, ev_all, (self.flags, epoch)
+        return k_all, v_all, ev_local, ev_all, (self.flags, epoch, per)
 
     def gather(self, rows: int, kv0: int, k_g: torch.Tensor, v_g: torch.Tensor):
         """This rank's [n_local*128, nkv, d] K/V slice of the KV heads
@@ -529,13 +548,14 @@ def cp_forward(q_loc, k_loc, v_loc, plan: CPPlan, group=None, scale=None, groups
         # order the pulls land
         comm.wait_stream(cur)
         with torch.cuda.stream(comm):
-            k_all, v_all, ev_local, ev_all, (flags, epoch) = ex.gather_overlapped(
+            k_all, v_all, ev_local, ev_all, (flags, epoch, flag_heads) = ex.gather_overlapped(
                 rows, k_loc, v_loc)
         cur.wait_event(ev_local)
         k_all.record_stream(cur)
         v_all.record_stream(cur)
         A.attn_forward(q_loc, k_all, v_all, plan.attn, scale, out=(o, lse),
-                       kv_ready=(flags, epoch, plan.layout.rank, plan.layout.max_blocks),
+                       kv_ready=(flags, epoch, plan.layout.rank, plan.layout.max_blocks,
+                                 flag_heads),
                        kv_head_major=True, timer=timer)
         cur.wait_event(ev_all)
         return o, lse, [(k_all, v_all)]

@@ -43,6 +43,14 @@ __device__ __forceinline__ void load_tile(const CUtensorMap* m, uint64_t* bar, u
   tma_load_3d(m, bar, dst + kTileBytes / 2, 64, head, row0);
 }
 
+// The CP arrival flag guarding rank `owner`'s rows of KV head hkv
+// (BamAttnFwdParams.kv_ready / kv_head_major / kv_flag_heads)
+__device__ __forceinline__ int kv_flag_index(const BamAttnFwdParams& p, int owner, int hkv) {
+  if (!p.kv_head_major) return owner;
+  const int g = p.kv_flag_heads > 1 ? p.kv_flag_heads : 1;
+  return owner * p.Hkv + (hkv / g) * g;
+}
+
 // One CTA's work: a whole query-block row (items == NULL: heavy-first order)
 // or a split-KV subblock [first, end) of its tile list (LPT-ordered items).
 struct WorkItem {
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           const int owner = kblk / p.kv_rows_per_rank;
           if (owner != p.kv_rank && !((ready >> owner) & 1)) {
             if (lane == 0)
-              wait_flag_geq(p.kv_ready + (p.kv_head_major ? owner * p.Hkv + hkv : owner),
+              wait_flag_geq(p.kv_ready + kv_flag_index(p, owner, hkv),
                             p.kv_epoch);
             __syncwarp();
             fence_proxy_async_global();
@@ -712,7 +720,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
             const unsigned long long w0 = bam_globaltimer();
 #endif
             if (lane == 0)
-              wait_flag_geq(p.kv_ready + (p.kv_head_major ? owner * p.Hkv + hkv : owner),
+              wait_flag_geq(p.kv_ready + kv_flag_index(p, owner, hkv),
                             p.kv_epoch);
             __syncwarp();
             fence_proxy_async_global();  // the copy engine's data before the TMA reads
@@ -1054,7 +1062,8 @@ using namespace bam;
   BAM_CHECK_ARG(!(p).kv_ready ||                                                           \
                     ((p).kv_rows_per_rank >= 1 &&                                          \
                      ((p).k_rows + (p).kv_rows_per_rank - 1) / (p).kv_rows_per_rank <= 64 && \
-                     (p).kv_rank >= 0 && (p).kv_rank < 64),                                \
+                     (p).kv_rank >= 0 && (p).kv_rank < 64 && (p).kv_flag_heads >= 0 &&     \
+                     ((p).kv_flag_heads <= 1 || (p).Hkv % (p).kv_flag_heads == 0)),         \
                 fn ": kv_ready needs kv_rows_per_rank >= 1 and at most 64 ranks "          \
                    "(kv_rows_per_rank=%d k_rows=%d kv_rank=%d)",                           \
                 (p).kv_rows_per_rank, (p).k_rows, (p).kv_rank)

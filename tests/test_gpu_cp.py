@@ -434,9 +434,12 @@ def test_cp_emulated_mha_overlapped_forward():
                 for h in range(Hkv):
                     k_all[h, sl].copy_(k_src_h[h, sl], non_blocking=True)
                     v_all[h, sl].copy_(v_src_h[h, sl], non_blocking=True)
-                    _lib.call("bam_stream_write_i32", flags[peer * Hkv + h:].data_ptr(), epoch)
+                    if h % 2 == 1:                # one flag per pair of KV heads
+                        _lib.call("bam_stream_write_i32", flags[peer * Hkv + h - 1:].data_ptr(),
+                                  epoch)
         o, lse = A.attn_forward(q_loc, k_all, v_all, plan.attn,
-                                kv_ready=(flags, epoch, rank, lay.max_blocks), kv_head_major=True)
+                                kv_ready=(flags, epoch, rank, lay.max_blocks, 2),
+                                kv_head_major=True)
         torch.cuda.synchronize()
         ws = A.BackwardWorkspace(q_loc, o, lse, do_loc, plan.attn, None)
         dk_all, dv_all = ws.main(k_all, v_all, kv_head_major=True)

@@ -53,10 +53,10 @@ rs_bytes = (world - 1) * rows * Hkv * D * 4 * 2              # fp32 dK and dV to
 steps = {
     ("kv_all_gather", "nccl"): (lambda: cp.gather_kv(k_loc, v_loc, lay), gather_bytes),
     ("kv_all_gather", "ce"): (lambda: ex.gather(rows, 0, k_loc, v_loc), gather_bytes),
-    ("kv_all_gather", "ce_overlapped_1stream"): (
-        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 1), gather_bytes),   # bench.py's
     ("kv_all_gather", "ce_overlapped_2streams"): (
-        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 2), gather_bytes),
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 2), gather_bytes),   # bench.py's
+    ("kv_all_gather", "ce_overlapped_1stream"): (
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 1), gather_bytes),
     ("kv_all_gather", "ce_overlapped_4streams"): (
         lambda: ex.gather_overlapped(rows, k_loc, v_loc, 4), gather_bytes),
     ("kv_all_gather", "ce_overlapped_8streams"): (
