@@ -186,7 +186,7 @@ class SymmExchange:
         # one stream per peer so the copies run on several copy engines at once
         self.streams = [torch.cuda.Stream(device=device) for _ in range(self.world)]
         self.flags, self.epoch = None, 0   # gather_overlapped's arrival flags
-        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "2"))   # pull streams
+        self.head_chunks = int(os.environ.get("BAM_CP_HEAD_CHUNKS", "1"))   # pull streams
         self._cache = {}
 
     def _check(self, rows: int, kv0: int, nkv: int):
@@ -225,10 +225,10 @@ class SymmExchange:
         copy (``bam_copy_2d``) followed by one stream-ordered flag store per
         (peer, group) ``flags[peer*nkv + h0] = epoch`` (bam_stream_write_i32, no
         SM; ``kv_flag_heads`` = the group size) that the forward kernel waits on
-        per tile.  Every rank pulls from a different peer
-        at a time; two streams joined per peer (the default) measured 556-560 GB/s
-        per rank at N=4, one stream 525-535 (per-head copies from all peers at
-        once: 300-367, tools/exchange_bw.py).
+        per tile.  Every rank pulls from a different peer at a time; one stream
+        and one flag per peer (the default) measured 581 GB/s per rank at N=4,
+        two streams joined per peer 551 (per-head copies and flags from all
+        peers at once: 300-367, tools/exchange_bw.py).
         ``ev_all``: every pull landed.
         Returns (k_all, v_all, ev_local, ev_all, (flags, epoch, heads per flag))."""
         nkv, d = k_g.shape[1], self.d
@@ -258,8 +258,7 @@ class SymmExchange:
         dpitch = self.world * row_b
 
         # peer by peer: the `chunks` streams pull one peer's head groups together and
-        # join before the next peer (without the join they drift onto different peers
-        # and measured 482-520 instead of 556-560 GB/s per rank at N=4 on two streams)
+        # join before the next peer (without the join they drift onto different peers)
         while len(self.streams) < chunks:
             self.streams.append(torch.cuda.Stream(device=cur.device))
         prev = torch.cuda.Event()
