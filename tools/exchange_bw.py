@@ -9,7 +9,8 @@ shards, through both transports: "nccl" (cp.gather_kv / cp.scatter_dkv) and
 "ce" (cp.SymmExchange copy-engine pulls / pushes over torch symmetric
 memory, its device barriers included), plus "ce_overlapped_<k>streams" = the
 gather_overlapped() pulls bench.py uses (peer by peer in rotation order on k
-streams, one group of KV heads each; k = 2 by default) and
+streams joined per peer, one group of KV heads and one arrival flag each;
+k = 1 by default) and
 "ce_peer_sequential_<k>" (the same with a join between peers).  Prints one JSON line per
 (step, transport): peer bytes per rank (what crosses NVLink into, for the
 gather, or out of, for the reduce-scatter, one GPU) and that over the time.
@@ -53,10 +54,10 @@ rs_bytes = (world - 1) * rows * Hkv * D * 4 * 2              # fp32 dK and dV to
 steps = {
     ("kv_all_gather", "nccl"): (lambda: cp.gather_kv(k_loc, v_loc, lay), gather_bytes),
     ("kv_all_gather", "ce"): (lambda: ex.gather(rows, 0, k_loc, v_loc), gather_bytes),
-    ("kv_all_gather", "ce_overlapped_2streams"): (
-        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 2), gather_bytes),   # bench.py's
     ("kv_all_gather", "ce_overlapped_1stream"): (
-        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 1), gather_bytes),
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 1), gather_bytes),   # bench.py's
+    ("kv_all_gather", "ce_overlapped_2streams"): (
+        lambda: ex.gather_overlapped(rows, k_loc, v_loc, 2), gather_bytes),
     ("kv_all_gather", "ce_overlapped_4streams"): (
         lambda: ex.gather_overlapped(rows, k_loc, v_loc, 4), gather_bytes),
     ("kv_all_gather", "ce_overlapped_8streams"): (
