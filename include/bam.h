@@ -197,10 +197,11 @@ int bam_attn_fwd(const BamAttnFwdParams* p, void* stream);
 int bam_attn_fwd_combine(const BamAttnFwdParams* p, const int32_t* combine, int32_t n_combine,
                          void* stream);
 
-/* Backward.  dq (bf16) for the local rows; dk/dv fp32 partial gradients for
- * every key row of k/v (the contributions of the local queries; summed over
- * CP ranks by a reduce-scatter).  delta ([Hq, 2, nq*128] fp32) and dq_acc
- * ([nq*128, Hq, 128] fp32) are caller workspaces. */
+/* Backward.  dq (bf16) for the local rows; dk/dv for every key row of k/v:
+ * fp32 partial gradients (the contributions of the local queries, summed over
+ * CP ranks by a reduce-scatter) or, with dkv_bf16, the complete bf16 gradients
+ * (one GPU).  delta ([Hq, 2, nq*128] fp32) and dq_acc ([Hq, nq*128, 128] fp32,
+ * head-major) are caller workspaces. */
 typedef struct BamAttnBwdParams {
   const void* q;
   const void* k;
