@@ -607,6 +607,8 @@ def test_copy_2d_and_kv_ready_validation():
         A.attn_forward(q, k, k, plan, kv_ready=(flags, 1, 0, 0))
     with pytest.raises(ValueError, match="kv_ready"):
         A.attn_forward(q, k, k, plan, kv_ready=(flags, 1, 70, 1))
+    with pytest.raises(_lib.BamError, match="kv_ready"):   # flag groups must divide Hkv
+        A.attn_forward(q, k, k, plan, kv_ready=(flags, 1, 0, 512, 3))
     # a rank that owns no query block cannot run (more ranks than blocks)
     with pytest.raises(ValueError, match="owns no query block"):
         cp.make_cp_plan(mask, 16, 15, "zigzag")
