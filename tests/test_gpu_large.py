@@ -110,3 +110,53 @@ def _full_size_parity(segments, Hq, Hkv):
             dk_ref[:, hk] += (ds.t() @ Qh) * scale
         check(f"dK[kb={kb}]", dk.cpu()[keys], dk_ref)
         check(f"dV[kb={kb}]", dv.cpu()[keys], dv_ref)
+
+
+def test_full_dkdv_one_kv_group_config4():
+    """SURVEY.md 8(d)'s full-size recipe for dK/dV: the complete dK and dV of one
+    KV-head group (the last one: 4 query heads) at config 4 (128K), against an
+    independent fp32 oracle pass -- its own forward (O, LSE) and backward per
+    query block, blockwise-sparse over that row's non-skip key tiles
+    (PAPER.md:616-619), the contributions summed at their key positions."""
+    from paper_2503_11367_b200 import attention as A, mask as M
+    from paper_2503_11367_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[4]
+    Hq, Hkv = cfg["Hq"], cfg["Hkv"]
+    grp, hk = Hq // Hkv, Hkv - 1
+    mask = M.build_bitfield(cfg["segments"])
+    desc_d = mask.device_descriptors()
+    T = desc_d.shape[0]
+    nb = T // 128
+    desc = desc_d.cpu().numpy()
+    plan = A.build_plan(desc_d)
+    cls = plan.classes.cpu().numpy()
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(4321)
+    q = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    k = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    v = torch.randn(T, Hkv, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    do = torch.randn(T, Hq, 128, device=dev, generator=g, dtype=torch.bfloat16)
+    o, lse = A.attn_forward(q, k, v, plan)
+    _, dk, dv = A.attn_backward(q, k, v, o, lse, do, plan, dkv_fp32=True)
+    torch.cuda.synchronize()
+    heads = slice(hk * grp, (hk + 1) * grp)
+    qg, dog = q[:, heads].cpu(), do[:, heads].cpu()
+    kg, vg = k[:, hk:hk + 1].cpu(), v[:, hk:hk + 1].cpu()
+    dk_ref = torch.zeros(T, 128)
+    dv_ref = torch.zeros(T, 128)
+    for j in range(nb):
+        kbs = np.nonzero(cls[j])[0]
+        if kbs.size == 0:
+            continue
+        keys = np.concatenate([np.arange(b * 128, (b + 1) * 128) for b in kbs])
+        rows = np.arange(j * 128, (j + 1) * 128)
+        kt, rt = torch.from_numpy(keys), torch.from_numpy(rows)
+        o_r, lse_r = attention_ref.attention_fwd(qg[rt], kg[kt], vg[kt], desc, rows, chunk=128,
+                                                 k_pos=keys)
+        _, dk_r, dv_r = attention_ref.attention_bwd(qg[rt], kg[kt], vg[kt], o_r, lse_r, dog[rt],
+                                                    desc, rows, chunk=128, k_pos=keys)
+        dk_ref[kt] += dk_r[:, 0]
+        dv_ref[kt] += dv_r[:, 0]
+    check(f"dK[kv head {hk}, all {T} keys]", dk.cpu()[:, hk], dk_ref)
+    check(f"dV[kv head {hk}, all {T} keys]", dv.cpu()[:, hk], dv_ref)
